@@ -1,0 +1,32 @@
+# Builds the product library (sm_100a) and the test-only oracle libraries.
+#   make            -> paper_2306_07629_b200/libdsq_cuda.so + oracle/liboracle.so (+ oracle/_ref if /root/reference exists)
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas -v
+PKG       := paper_2306_07629_b200
+CSRC      := $(PKG)/csrc
+LIB       := $(PKG)/libdsq_cuda.so
+OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/api.o
+
+all: $(LIB) oracle
+
+$(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/layout.hpp $(CSRC)/ptx.cuh
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/kernels.ptxas.log || (cat $(CSRC)/kernels.ptxas.log; false)
+
+$(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layout.hpp
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/stack.ptxas.log || (cat $(CSRC)/stack.ptxas.log; false)
+
+$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/layout.hpp $(CSRC)/stack.hpp include/dsq_cuda.h
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC,-fopenmp -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(OBJS) $(LIB) $(CSRC)/*.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

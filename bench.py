@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""bench.py -- SqueezeLLM Dense-and-Sparse LUT-GEMV hot path on B200.
+
+Workload (BASELINE.json configs[1], LLaMA-7B shapes, batch 1): one STEP is the
+linear GEMV chain of one LLaMA-7B decoder layer, every GEMV a 3-bit LUT +
+0.45% CSR fused product (the hot path):
+    q,k,v,o : 4096 x 4096     gate,up : 11008 x 4096     down : 4096 x 11008
+chained through fp16 outputs (v,q,k read the step input; o reads v; up,gate
+read o; down reads up).  Each step uses a different decoder layer's weights out of a rotation
+whose working set (>1 GB) is far larger than L2.
+
+Steps are chained like consecutive decoder layers: the q/k/v input of step t
+is the down output of step t-1 (attention, norms and residuals are out of
+scope and are not computed).
+
+  value  = effective HBM GB/s = reference-charged bytes of the 7 GEMVs
+           (bytes_touched_estimate, kernels.cpp:205-212) / device time
+  e2e    = same metric through the reference-facing host call
+           (dsq_cuda_matvec_host: fp32 host x -> fp64 host y, per GEMV)
+  --impl reference : the reference's own CPU fused_dns_matvec (compiled from
+           /root/reference sources into oracle/_ref), all host threads.
+
+Multi-GPU (torchrun, one process per GPU): replicas -- each rank streams its
+own decoder layers (weak scaling, no data-path collective in this round).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LUT-GEMV µs/layer & effective HBM GB/s (% of peak); decode tok/s at 1/2/4/8"
+# One decoder layer's GEMVs in dependency-aware issue order: v first so that o
+# (which consumes the attention output, stood in for by v's output) does not
+# wait; up before gate so that down (stand-in input: up's output) does not wait.
+SHAPES = [("v", 4096, 4096), ("q", 4096, 4096), ("k", 4096, 4096), ("o", 4096, 4096),
+          ("up", 11008, 4096), ("gate", 11008, 4096), ("down", 4096, 11008)]
+# input of each GEMV (index into this step's outputs; -1 = the step input,
+# which is the previous step's down output -- steps chain like decoder layers)
+CHAIN_IN = [-1, -1, -1, 0, 3, 3, 4]
+BITS, SPARSITY = 3, 0.0045
+LLAMA7B_LAYERS = 32
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def workload_config(n_rot: int, parallelism: str) -> dict:
+    return {
+        "workload": "llama7b-decoder-linear-chain: q,k,v,o 4096x4096; gate,up 11008x4096; "
+                    "down 4096x11008; 3-bit LUT (8 fp16 centroids/row) + 0.45% CSR fp16 "
+                    "outliers; batch 1 (BASELINE configs[1])",
+        "gemvs_per_step": len(SHAPES),
+        "bits": BITS, "sparsity": SPARSITY, "batch": 1,
+        "l2": f"inputs larger than L2: rotation over {n_rot} decoder layers of distinct "
+              f"device weights",
+        "parallelism": parallelism,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons, pw = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for n, v in zip(names, r[2:6]):
+                    if v.strip().lower() in ("active", "1"):
+                        reasons.add(n)
+                pw.append(float(r[6]))
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+# CPU (reference) leg
+# ---------------------------------------------------------------------------
+def slice_rows(L, r0, r1):
+    from oracle.oracle import Layer
+    k = 1 << L.bits
+    stride = (L.cols * L.bits + 7) // 8
+    a, b = int(L.row_ptr[r0]), int(L.row_ptr[r1])
+    return Layer(L.bits, r1 - r0, L.cols, L.assign[r0 * L.cols:r1 * L.cols],
+                 L.luts16[r0 * k:r1 * k], L.payload[r0 * stride:r1 * stride],
+                 (L.row_ptr[r0:r1 + 1] - a).astype(np.uint32), L.col_idx[a:b],
+                 L.values16[a:b])
+
+
+def cpu_reference_sample(host_layers, frac: float, repeats: int = 3):
+    """Time the reference's fused_dns_matvec (OpenMP, all host threads) through
+    its own bench_matvec (median of `repeats` after one warmup) on a row slice
+    of every GEMV of one decoder layer.  Returns (GB/s, seconds, bytes, cores, desc)."""
+    from oracle.oracle import Reference, make_x
+    ref = Reference()
+    cores = os.cpu_count() or 1
+    ref.lib.ref_set_threads(cores)
+    total_s, total_b = 0.0, 0
+    for (name, rows, cols), L in zip(SHAPES, host_layers):
+        n = max(32, int(rows * frac))
+        Ls = slice_rows(L, 0, n)
+        rl = ref.layer(Ls, top_k=10)
+        med, bt = rl.bench("fused", make_x(cols).astype(np.float32), repeats=repeats)
+        total_s += med
+        total_b += bt
+    desc = (f"reference dsq::fused_dns_matvec via dsq::bench_matvec (median of {repeats} after "
+            f"1 warmup, OpenMP {cores} threads) on the first {frac:.4g} of the rows of each of "
+            f"the 7 GEMVs of one decoder layer ({total_b} charged bytes)")
+    return total_b / total_s / 1e9, total_s, total_b, cores, desc
+
+
+def build_host_layers(seed: int = 1234):
+    from oracle.oracle import make_layer
+    cache = {}
+    out = []
+    for name, rows, cols in SHAPES:
+        key = (rows, cols)
+        if key not in cache:
+            cache[key] = make_layer(rows, cols, BITS, SPARSITY, seed=seed + rows + cols)
+        out.append(cache[key])
+    return out
+
+
+def run_reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return
+    t0 = time.time()
+    host_layers = build_host_layers()
+    frac = args.ref_frac
+    for _ in range(args.warmup):
+        cpu_reference_sample(host_layers, frac, repeats=3)
+    vals, secs, byts = [], 0.0, 0
+    cores, desc = 1, ""
+    for _ in range(args.steps):
+        v, s, b, cores, desc = cpu_reference_sample(host_layers, frac, repeats=3)
+        vals.append(v)
+        secs += s
+        byts += b
+    value = byts / secs / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(1, "cpu"),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores,
+                         "kind": "reference", "sample": desc},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(time.time() - t0, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    import paper_2306_07629_b200._native as N
+    from paper_2306_07629_b200 import DeviceLayer
+    from oracle.oracle import make_x, to_quantized_layer
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    t_setup = time.time()
+    host_layers = build_host_layers()
+    qls = [to_quantized_layer(L, name=n) for L, (n, _, _) in zip(host_layers, SHAPES)]
+    bytes_step = sum(int(N.lib.dsq_bytes_touched_estimate(r, c, BITS, 0, L.nnz))
+                     for L, (_, r, c) in zip(host_layers, SHAPES))
+    n_rot = args.rotation
+    # n_rot decoder layers of distinct device weights
+    dls = [[DeviceLayer(q, device=local_rank) for q in qls] for _ in range(n_rot)]
+    info = dls[0][0].info()
+    # graphs must be captured on a non-default stream; everything runs on it
+    st = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(st)
+    sp = st.cuda_stream
+    # activations: step input x (fp16) + 7 fp16 outputs, one set per rotation slot
+    xs = [torch.from_numpy(make_x(4096, seed=100 + i).view(np.int16)).to(dev)
+          for i in range(n_rot)]
+    ys = [[torch.empty(r, dtype=torch.int16, device=dev) for (_, r, _) in SHAPES]
+          for _ in range(n_rot)]
+
+    def step_input(slot: int, first: bool):
+        return xs[slot] if first else ys[(slot - 1) % n_rot][len(SHAPES) - 1]
+
+    def launch_step(slot: int, first: bool = False):
+        outs = ys[slot]
+        for j, ((_, r, c), dl) in enumerate(zip(SHAPES, dls[slot])):
+            src = step_input(slot, first) if CHAIN_IN[j] < 0 else outs[CHAIN_IN[j]]
+            dl.gemv(N.KERNEL_FUSED, src.data_ptr(), N.F16, outs[j].data_ptr(), N.F16, sp)
+
+    # eager warm-up (sets kernel attributes, first-touch)
+    for s in range(max(1, args.warmup)):
+        launch_step(s % n_rot, first=(s == 0))
+    torch.cuda.synchronize()
+
+    if args.mode == "graph":
+        # one launch per GEMV (programmatic dependent launch), captured in a CUDA graph
+        def capture(nsteps: int, offset: int):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for s in range(nsteps):
+                    launch_step((offset + s) % n_rot, first=(s == 0))
+            return g
+
+        g_warm, g_time = capture(args.warmup, 0), capture(args.steps, args.warmup)
+        run_warm, run_time = g_warm.replay, g_time.replay
+        launches = args.steps * len(SHAPES)
+        kernel_name = "sqz::stack_gemv<3> (1 layer per launch)"
+    else:
+        # ONE persistent launch runs all K steps (K*7 chained GEMVs)
+        from paper_2306_07629_b200 import DeviceStack
+
+        def build_stack(nsteps: int, offset: int):
+            layers, deps, xp, yp = [], [], [], []
+            prev_down = -1
+            for s in range(nsteps):
+                slot = (offset + s) % n_rot
+                base = len(layers)
+                for j, dl in enumerate(dls[slot]):
+                    layers.append(dl)
+                    if CHAIN_IN[j] < 0 and prev_down < 0:
+                        deps.append(-1)
+                        xp.append(xs[slot].data_ptr())
+                    else:
+                        deps.append(prev_down if CHAIN_IN[j] < 0 else base + CHAIN_IN[j])
+                        xp.append(0)
+                    yp.append(ys[slot][j].data_ptr())
+                prev_down = base + len(SHAPES) - 1
+            return DeviceStack(layers, deps, xp, yp, N.F16)
+
+        s_warm, s_time = build_stack(args.warmup, 0), build_stack(args.steps, args.warmup)
+        run_warm = lambda: s_warm.run(sp)  # noqa: E731
+        run_time = lambda: s_time.run(sp)  # noqa: E731
+        launches = 1
+        kernel_name = "sqz::stack_gemv<3> (persistent, all K*7 GEMVs in one launch)"
+    run_warm()
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+
+    # soak: keep the GPU under load while the clock sampler runs
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    t_end = time.time() + args.soak
+    while time.time() < t_end:
+        run_warm()
+        torch.cuda.synchronize()
+    # W untimed warm-up steps, then exactly K timed steps
+    run_warm()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    run_time()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * bytes_step * args.steps / (ms * 1e-3) / 1e9
+    us_layer = ms_step * 1e3 / len(SHAPES)
+
+    # ---- e2e: the reference-facing host call (fp32 host x -> fp64 host y)
+    e2e = None
+    if not args.no_e2e:
+        n_e2e = min(args.steps, args.e2e_steps)
+        xh = torch.empty(4096, dtype=torch.float32).pin_memory().numpy()
+        xh[:] = make_x(4096).astype(np.float32)
+        big = torch.empty(11008, dtype=torch.float32).pin_memory().numpy()
+
+        def e2e_step(slot):
+            outs = []
+            for j, ((_, r, c), dl) in enumerate(zip(SHAPES, dls[slot])):
+                if CHAIN_IN[j] < 0:
+                    src = xh
+                else:
+                    src = big[:c]
+                    src[:] = outs[CHAIN_IN[j]]
+                y = dl.matvec_host(N.KERNEL_FUSED, src)
+                outs.append(y.astype(np.float32))
+            return outs
+
+        for s in range(2):
+            e2e_step(s % n_rot)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(n_e2e):
+            e2e_step(s % n_rot)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": round(world * bytes_step * n_e2e / el / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": sum(c * 4 for (_, _, c) in SHAPES),
+               "d2h_bytes_per_step": sum(r * 4 for (_, r, _) in SHAPES),
+               "steps": n_e2e, "ms_per_step": round(el / n_e2e * 1e3, 3),
+               "api": "dsq_cuda_matvec_host per GEMV (the fused_dns_matvec(layer, x) "
+                      "host-vector signature)"}
+
+    if rank != 0:
+        return
+    pk = peaks()
+    peak = float(pk.get("hbm_gbs", 6650.0))
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+    per_rank = value / world
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic (random fp16 centroids/indices/deltas; weights random-init)",
+        "config": workload_config(n_rot, "tp1" if world == 1 else f"replicas{world}"),
+        "us_per_layer": round(us_layer, 3),
+        "decode_tok_s_linear": round(1e3 / (ms_step * LLAMA7B_LAYERS), 1),
+        "frac_of_8TBs": round(per_rank / 8000.0, 4),
+        "roofline": {"bound": "hbm", "achieved": round(per_rank, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(per_rank / peak, 4), "traffic": traffic,
+                     "kernel": kernel_name,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback",
+                     "algorithmic_bytes_per_step": bytes_step},
+        "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+        "gemvs_timed": args.steps * len(SHAPES), "mode": args.mode,
+        "schedule": {"workers": info.workers, "ctas": info.ctas},
+        "setup_s": round(setup_s, 1),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        v, s, b, cores, desc = cpu_reference_sample(host_layers, args.ref_frac, repeats=3)
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": cores,
+                                "kind": "reference", "sample": desc}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["stack", "graph"], default="stack",
+                    help="stack: one persistent launch for all K steps; graph: one launch "
+                         "per GEMV captured in a CUDA graph")
+    ap.add_argument("--rotation", type=int, default=16,
+                    help="decoder layers of distinct device weights (working set >> L2)")
+    ap.add_argument("--soak", type=float, default=1.0, help="seconds of load before timing")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-frac", type=float, default=1 / 16,
+                    help="row fraction of each GEMV in the CPU sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

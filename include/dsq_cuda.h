@@ -1,0 +1,216 @@
+/*
+ * dsq_cuda.h -- C ABI of the B200 (sm_100a) Dense-and-Sparse LUT-GEMV hot path.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/dsq/kernels.hpp:17-79).  Every entry point
+ * below names the reference interface it replaces.  Plain pointers and sizes
+ * only; no C++ or torch types cross this boundary; no exception crosses it.
+ *
+ * Ownership: layer views are non-owning and only read during
+ * dsq_cuda_layer_create (pack/re-tile + upload happen once).  The returned
+ * layer handle owns all of its device memory.  Caller owns x / y buffers and
+ * the stream.  All gemv calls are stream-ordered and asynchronous, and
+ * deterministic (no floating-point atomics): a given layer on a given device
+ * produces bit-identical outputs on every call.
+ *
+ * Numerics: LUT centroids, CSR values and activations are fp16 on device
+ * (the reference stores fp32 but charges 16 bits: SPEC.md:75, 231).
+ * Products are exact (fp16 x fp16 -> fp32), accumulation is fp32.
+ */
+#ifndef DSQ_CUDA_H
+#define DSQ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSQ_CUDA_ABI_VERSION 1
+
+/* Status codes.  1..15 mirror dsq::errc in declaration order
+ * (reference include/dsq/common.hpp:13-29), so a C++ wrapper can rethrow
+ * dsq::Error{errc(status-1)} and keep the CLI exit-code mapping of
+ * tools/dsq.cpp:399-411 (argument->2, data->3, internal->4). */
+typedef enum dsq_status {
+    DSQ_OK = 0,
+    DSQ_E_MISSING_FILE = 1,
+    DSQ_E_MALFORMED_HEADER = 2,
+    DSQ_E_NON_FINITE_VALUE = 3,
+    DSQ_E_EMPTY_DIMENSION = 4,
+    DSQ_E_DIMENSION_OVERFLOW = 5,
+    DSQ_E_TRUNCATED_PAYLOAD = 6,
+    DSQ_E_CHECKSUM_MISMATCH = 7,
+    DSQ_E_UNSUPPORTED_VERSION = 8,
+    DSQ_E_SHAPE_MISMATCH = 9,
+    DSQ_E_EMPTY_INPUT = 10,
+    DSQ_E_INVALID_ARGUMENT = 11,
+    DSQ_E_FRACTION_OVERFLOW = 12,
+    DSQ_E_EMPTY_CHANNEL = 13,
+    DSQ_E_IO_FAILURE = 14,
+    DSQ_E_INTERNAL = 15,
+    /* device-side failures (no reference counterpart) */
+    DSQ_E_CUDA = 100,
+    DSQ_E_NO_DEVICE = 101,
+    DSQ_E_UNSUPPORTED = 102
+} dsq_status;
+
+/* element types for x / y */
+typedef enum dsq_dtype { DSQ_F32 = 0, DSQ_F16 = 1, DSQ_F64 = 2 } dsq_dtype;
+
+/* kernel selector, mirrors dsq::BenchKernel (kernels.hpp:71) */
+typedef enum dsq_kernel {
+    DSQ_KERNEL_LUT = 0,       /* lut_matvec: dense LUT part only        */
+    DSQ_KERNEL_CSR = 1,       /* csr_matvec: sparse deltas only          */
+    DSQ_KERNEL_FUSED = 2,     /* fused_dns_matvec: LUT + CSR, one launch */
+    DSQ_KERNEL_REFERENCE = 3  /* fp16 dense GEMV on the dequantized W    */
+} dsq_kernel;
+
+/* Non-owning view of dsq::PackedDense (packfmt.hpp:16-33): the reference
+ * layout -- per-row LSB-first index bitstream, row_stride = ceil(cols*bits/8)
+ * bytes, LUT rows*groups_per_row*2^bits centroids.  Exactly one of
+ * luts_f32 / luts_f16 must be non-null. */
+typedef struct dsq_packed_view {
+    uint32_t bits;
+    uint32_t rows;
+    uint32_t cols;
+    uint32_t groups_per_row;
+    const float* luts_f32;
+    const uint16_t* luts_f16; /* IEEE binary16 bit patterns */
+    const uint8_t* payload;
+    size_t payload_len;       /* must equal rows * row_stride */
+} dsq_packed_view;
+
+/* Non-owning view of dsq::CsrMatrix (dns.hpp:14-24).  values are the DELTAS
+ * (original - lut_row[0]) written by quantize_layer (pipeline.cpp:25-32).
+ * Exactly one of values_f32 / values_f16 must be non-null (may both be null
+ * when nnz == 0). */
+typedef struct dsq_csr_view {
+    uint32_t rows;
+    uint32_t cols;
+    uint32_t nnz;
+    const uint32_t* row_ptr; /* rows + 1 */
+    const uint16_t* col_idx; /* nnz, strictly increasing per row */
+    const float* values_f32;
+    const uint16_t* values_f16;
+} dsq_csr_view;
+
+/* Non-owning view of dsq::QuantizedLayer (packfmt.hpp:50-61).  The hybrid
+ * split (dns.hpp:55-62) is not passed: it is a deterministic function of
+ * `sparse` (container.cpp:138-139) and the device schedule balances outlier
+ * skew itself, so fused == fused(top_k=0) == fused(top_k). */
+typedef struct dsq_layer_view {
+    const char* name;
+    uint32_t rows;
+    uint32_t cols;
+    dsq_packed_view packed;
+    dsq_csr_view sparse;
+    uint32_t hybrid_top_k; /* recorded for accounting only */
+} dsq_layer_view;
+
+typedef struct dsq_cuda_layer dsq_cuda_layer;
+
+/* Layer facts after upload. */
+typedef struct dsq_layer_info {
+    uint32_t rows, cols, bits, groups_per_row, nnz;
+    uint64_t device_bytes;      /* all device allocations of the handle      */
+    uint64_t algorithmic_bytes; /* bytes_touched_estimate (kernels.cpp:205)  */
+    uint32_t luts_exact_f16;    /* 1 if every centroid was fp16-representable */
+    uint32_t values_exact_f16;  /* 1 if every CSR delta was fp16-representable */
+    uint32_t workers;           /* warps in the balanced schedule              */
+    uint32_t ctas;              /* grid size of the fused launch               */
+} dsq_layer_info;
+
+/* ---- library ---------------------------------------------------------- */
+int dsq_cuda_abi_version(void);
+/* thread-local message for the last non-OK status (never NULL) */
+const char* dsq_cuda_last_error(void);
+
+/* ---- layer lifetime ----------------------------------------------------- */
+/* Validates the view exactly like QuantizedLayer::validate()
+ * (packfmt.cpp:82-92, dns.cpp:10-29) -- once, here, not per call (the
+ * reference validates inside every product, kernels.cpp:52,70,110) --
+ * re-tiles the index stream for coalesced per-warp tiles, converts LUTs and
+ * deltas to fp16, builds the balanced work schedule and uploads. */
+int dsq_cuda_layer_create(const dsq_layer_view* view, int device, dsq_cuda_layer** out);
+int dsq_cuda_layer_destroy(dsq_cuda_layer* layer);
+int dsq_cuda_layer_get_info(const dsq_cuda_layer* layer, dsq_layer_info* info);
+
+/* ---- products (device buffers, stream-ordered) -------------------------- */
+/* y[r] (rows) = product of row r with x (cols).  x_dtype F32/F16 (F32 is
+ * rounded to fp16 on device), y_dtype F32/F16.  batch must be 1 in ABI v1.
+ * Replaces:
+ *   DSQ_KERNEL_LUT   -> dsq::lut_matvec        kernels.hpp:20 / kernels.cpp:51-67
+ *   DSQ_KERNEL_CSR   -> dsq::csr_matvec        kernels.hpp:24 / kernels.cpp:69-85
+ *   DSQ_KERNEL_FUSED -> dsq::fused_dns_matvec  kernels.hpp:31 / kernels.cpp:108-141
+ *   DSQ_KERNEL_REFERENCE -> dense_matvec over ref::dequant_dense (the
+ *       "reference" bench kernel, kernels.cpp:227-228,276-278); the dense
+ *       fp16 W is materialized on first use. */
+int dsq_cuda_gemv(const dsq_cuda_layer* layer, int kernel, const void* x, int x_dtype,
+                  void* y, int y_dtype, uint32_t batch, void* stream);
+/* convenience wrappers */
+int dsq_cuda_lut_gemv(const dsq_cuda_layer* layer, const void* x, int x_dtype, void* y,
+                      int y_dtype, uint32_t batch, void* stream);
+int dsq_cuda_csr_gemv(const dsq_cuda_layer* layer, const void* x, int x_dtype, void* y,
+                      int y_dtype, uint32_t batch, void* stream);
+int dsq_cuda_fused_gemv(const dsq_cuda_layer* layer, const void* x, int x_dtype, void* y,
+                        int y_dtype, uint32_t batch, void* stream);
+
+/* Plain fp16 dense GEMV (dsq::dense_matvec, kernels.hpp:35 / kernels.cpp:87-106)
+ * on a device row-major W[rows][cols]. */
+int dsq_cuda_dense_gemv(const uint16_t* w_f16, uint32_t rows, uint32_t cols, const void* x,
+                        int x_dtype, void* y, int y_dtype, void* stream);
+
+/* ---- host-buffer products (the reference-facing call) -------------------- */
+/* Same semantics as the reference entry points, which take a host
+ * std::vector<float> x and return a host std::vector<double> (kernels.hpp:20-32):
+ * x_host fp32 [cols] -> y_host fp64 [rows].  Includes the H2D copy of x, the
+ * launch and the D2H copy of y; synchronous on the layer's internal stream. */
+int dsq_cuda_matvec_host(const dsq_cuda_layer* layer, int kernel, const float* x_host,
+                         double* y_host);
+
+/* ---- debug / parity kernels ----------------------------------------------- */
+/* K5: device decode of the re-tiled index layout into the reference
+ * AssignmentVector order (unpack, packfmt.cpp:57-80): assign[rows*cols] u16 */
+int dsq_cuda_unpack(const dsq_cuda_layer* layer, uint16_t* assign_dev, void* stream);
+/* K6: device dequantization (ref::dequant_dense, kernels.cpp:149-159):
+ * w[rows*cols] as fp16 bit patterns (out_dtype F16) or fp32 (F32) */
+int dsq_cuda_dequant(const dsq_cuda_layer* layer, void* w_dev, int out_dtype, void* stream);
+
+/* ---- accounting --------------------------------------------------------- */
+/* bytes_touched_estimate (kernels.cpp:205-212): the algorithmic bytes of one
+ * fused product; group_size 0 = channel-wise (packfmt.cpp:98-121) */
+uint64_t dsq_bytes_touched_estimate(uint32_t rows, uint32_t cols, uint32_t bits,
+                                    uint32_t group_size, uint64_t nnz);
+
+/* ---- stack runner (decode-time chain of layers) --------------------------- */
+/* Runs n layers back to back on one stream with programmatic dependent
+ * launch, layer i reading x_i and writing y_i (device pointers, fp16 x,
+ * y dtype per y_dtype).  x_i may alias y_{i-1} (chained decode). */
+int dsq_cuda_gemv_many(dsq_cuda_layer* const* layers, uint32_t n, int kernel,
+                       const void* const* xs, int x_dtype, void* const* ys, int y_dtype,
+                       void* stream);
+
+/* ---- persistent stack (K7): a whole decode chain in ONE launch ----------- */
+/* Binds n layers (bits 3 or 4, same width, same device) into a dependency
+ * chain executed by one persistent kernel: layer i reads x_i -- either the
+ * external fp16 vector xs[i] (deps[i] < 0) or the output of layer deps[i]
+ * (< i; then y_dtype must be F16) -- and writes ys[i].  Weight streaming runs
+ * ahead across layer boundaries; each dependency is a grid-wide completion
+ * counter.  Buffers are bound at create time (like a CUDA graph); x/y
+ * contents may change between runs.  A layer must not overwrite a buffer
+ * that a layer it does not (transitively) depend on still reads.
+ * No reference counterpart: the reference runs one product per call
+ * (kernels.hpp:31); this is the decode-time caller of that product. */
+typedef struct dsq_cuda_stack dsq_cuda_stack;
+int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                          const void* const* xs, void* const* ys, int y_dtype,
+                          dsq_cuda_stack** out);
+int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
+int dsq_cuda_stack_destroy(dsq_cuda_stack* stack);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSQ_CUDA_H */

@@ -1,0 +1,18 @@
+"""B200-native (sm_100a) SqueezeLLM Dense-and-Sparse LUT-GEMV hot path.
+
+The product is ``libdsq_cuda.so`` (C ABI: include/dsq_cuda.h); this package is
+its Python binding plus a mirror of the reference ``dsq`` hot-path API
+(see dsq.py).  Importing fails loudly if the library has not been built.
+"""
+from ._native import DsqError, LIB_PATH, lib  # noqa: F401
+from .dsq import (  # noqa: F401
+    BenchKernel, BenchRecord, CsrMatrix, DeviceLayer, DeviceStack, Exec, PackedDense, QuantizedLayer,
+    bench_matvec, bytes_touched_estimate, csr_matvec, device_layer, fused_dns_matvec,
+    lut_matvec, row_stride,
+)
+
+__all__ = [
+    "DsqError", "Exec", "BenchKernel", "BenchRecord", "PackedDense", "CsrMatrix",
+    "QuantizedLayer", "DeviceLayer", "DeviceStack", "device_layer", "lut_matvec", "csr_matvec",
+    "fused_dns_matvec", "bench_matvec", "bytes_touched_estimate", "row_stride",
+]

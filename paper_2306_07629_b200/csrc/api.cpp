@@ -1,0 +1,906 @@
+// api.cpp -- the extern "C" boundary (include/dsq_cuda.h): validation,
+// re-tiling packer, balanced work scheduler, upload and launches.
+//
+// Validation mirrors the reference checks and error codes
+// (QuantizedLayer::validate packfmt.cpp:82-92, PackedDense::validate
+// packfmt.cpp:7-16, CsrMatrix::validate dns.cpp:10-29) but runs once at
+// upload instead of inside every product (kernels.cpp:52,70,110).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dsq_cuda.h"
+#include "layout.hpp"
+#include "stack.hpp"
+
+namespace sqz {
+size_t fused_smem_bytes(uint32_t bits);
+cudaError_t launch_fused(int mode, const LayerParams& P, const WorkTable& Wt, const uint16_t* x,
+                         void* y, bool y_f16, uint32_t ctas, cudaStream_t st, bool pdl);
+cudaError_t launch_dense(const uint16_t* w, uint32_t rows, uint32_t cols, const uint16_t* x,
+                         void* y, bool y_f16, int num_sms, cudaStream_t st, bool pdl);
+cudaError_t launch_decode(int mode, const LayerParams& P, void* out, cudaStream_t st);
+cudaError_t launch_f32_to_f16(const float* in, uint16_t* out, uint32_t n, cudaStream_t st,
+                              bool pdl);
+cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl);
+cudaError_t launch_decode_records(int mode, uint32_t bits, const uint32_t* rec, uint32_t rows,
+                                  uint32_t cols, uint32_t ng, uint32_t ngp, uint32_t rw,
+                                  void* out, cudaStream_t st);
+}  // namespace sqz
+
+using namespace sqz;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(DSQ_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                                          \
+    do {                                                        \
+        cudaError_t _e = (expr);                                \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);     \
+    } while (0)
+
+// --- IEEE binary16 <-> binary32 on the host (round to nearest even) --------
+uint16_t f32_to_f16(float f) {
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u;
+    const uint32_t absx = x & 0x7fffffffu;
+    if (absx >= 0x7f800000u) return uint16_t(sign | 0x7c00u | (absx > 0x7f800000u ? 0x200u : 0u));
+    if (absx >= 0x477ff000u) return uint16_t(sign | 0x7c00u);  // rounds to >= 65520 -> inf
+    if (absx < 0x38800000u) {                                   // fp16 subnormal / zero
+        if (absx < 0x33000000u) return uint16_t(sign);          // < 2^-25 -> 0
+        const uint32_t e = absx >> 23;
+        const uint32_t m = (absx & 0x7fffffu) | 0x800000u;
+        const uint32_t shift = 126u - e;  // 14..24
+        uint32_t h = m >> shift;
+        const uint32_t rem = m & ((1u << shift) - 1u);
+        const uint32_t half = 1u << (shift - 1);
+        if (rem > half || (rem == half && (h & 1u))) ++h;
+        return uint16_t(sign | h);
+    }
+    uint32_t h = ((absx - 0x38000000u) >> 13);
+    const uint32_t rem = absx & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+    return uint16_t(sign | h);
+}
+
+float f16_to_f32(uint16_t h) {
+    const uint32_t sign = uint32_t(h & 0x8000u) << 16;
+    uint32_t e = (h >> 10) & 0x1fu, m = h & 0x3ffu, x;
+    if (e == 0) {
+        if (m == 0) {
+            x = sign;
+        } else {
+            e = 113;
+            while (!(m & 0x400u)) {
+                m <<= 1;
+                --e;
+            }
+            x = sign | (e << 23) | ((m & 0x3ffu) << 13);
+        }
+    } else if (e == 31) {
+        x = sign | 0x7f800000u | (m << 13);
+    } else {
+        x = sign | ((e + 112u) << 23) | (m << 13);
+    }
+    float f;
+    std::memcpy(&f, &x, 4);
+    return f;
+}
+
+size_t row_stride(uint32_t cols, uint32_t bits) { return (size_t(cols) * bits + 7) / 8; }
+
+// index c of a reference-layout row (packfmt.cpp:40-53, LSB-first)
+inline uint32_t ref_index(const uint8_t* row, size_t stride, uint32_t c, uint32_t bits) {
+    const size_t bp = size_t(c) * bits;
+    const size_t byte = bp >> 3;
+    uint32_t v = row[byte];
+    if (byte + 1 < stride) v |= uint32_t(row[byte + 1]) << 8;
+    return (v >> (bp & 7)) & ((1u << bits) - 1u);
+}
+
+// pack the 32 indices of one (row, group) into `bits` words (layout.hpp)
+inline void encode_unit(const uint8_t* idx, uint32_t bits, uint32_t* w) {
+    if (bits == 3) {
+        for (int k = 0; k < 3; ++k) {
+            uint32_t v = 0;
+            for (int n = 0; n < 8; ++n) {
+                uint32_t nib = idx[8 * k + n] & 7u;
+                nib |= ((idx[24 + n] >> k) & 1u) << 3;
+                v |= nib << (4 * n);
+            }
+            w[k] = v;
+        }
+    } else if (bits == 4) {
+        for (int k = 0; k < 4; ++k) {
+            uint32_t v = 0;
+            for (int n = 0; n < 8; ++n) v |= uint32_t(idx[8 * k + n] & 15u) << (4 * n);
+            w[k] = v;
+        }
+    } else {
+        for (uint32_t k = 0; k < bits; ++k) w[k] = 0;
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t bp = uint32_t(j) * bits;
+            const uint64_t v = uint64_t(idx[j]) << (bp & 31);
+            w[bp >> 5] |= uint32_t(v);
+            if ((bp & 31) + bits > 32) w[(bp >> 5) + 1] |= uint32_t(v >> 32);
+        }
+    }
+}
+
+int query_num_sms(int device, int* out) {
+    int n = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+    *out = n;
+    return DSQ_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// persistent stack plan: shared-memory carve-up and per-layer chunking
+// ---------------------------------------------------------------------------
+namespace {
+
+struct StackPlanLayer {
+    uint32_t rows, cols, ng, ngp, rw, max_nnz_cta;
+};
+
+uint32_t max_nnz_per_cta(const std::vector<uint32_t>& rp, uint32_t rows, int G) {
+    uint32_t m = 0;
+    for (int c = 0; c < G; ++c) {
+        const uint32_t r0 = uint32_t((uint64_t(rows) * c) / G);
+        const uint32_t r1 = uint32_t((uint64_t(rows) * (c + 1)) / G);
+        m = std::max(m, rp[r1] - rp[r0]);
+    }
+    return m;
+}
+
+void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes) {
+    d.rows = l.rows;
+    d.cols = l.cols;
+    d.ng = l.ng;
+    d.ngp = l.ngp;
+    d.rw = l.rw;
+    d.chunk_rows = std::max<uint32_t>(1, slot_bytes / (l.rw * 4));
+    d.nslices = ceil_div(l.ng, 32);
+    d.dep = kNoDep;
+}
+
+int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
+               uint32_t& gseg_rounds) {
+    int dev = 0, smax = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    uint32_t max_ng = 0, max_rows = 0, max_sl = 0, max_nnz = 0, max_rec = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        max_ng = std::max(max_ng, Ls[i].ng);
+        max_rows = std::max(max_rows, ceil_div(Ls[i].rows, G));
+        max_sl = std::max(max_sl, ceil_div(Ls[i].ng, 32));
+        max_nnz = std::max(max_nnz, Ls[i].max_nnz_cta);
+        max_rec = std::max(max_rec, Ls[i].rw * 4);
+    }
+    auto al = [](size_t b, size_t a) { return (b + a - 1) / a * a; };
+    size_t off = 1024;  // mbarriers
+    sp.off_x = uint32_t(off);
+    sp.x_bytes = uint32_t(al(size_t(max_ng) * 64, 128));
+    off += 2 * size_t(sp.x_bytes);
+    sp.off_rp = uint32_t(off);
+    sp.rp_words = uint32_t(al(max_rows + 1, 32));
+    off += 2 * size_t(sp.rp_words) * 4;
+    sp.off_csr = uint32_t(off);
+    sp.csr_cap = uint32_t(al(std::min<uint32_t>(std::max<uint32_t>(max_nnz, 32), 2048), 32));
+    off += 2 * size_t(sp.csr_cap) * 4;
+    sp.off_part = uint32_t(off);
+    sp.part_stride = std::max<uint32_t>(max_sl, 1);
+    sp.part_rows = std::max<uint32_t>(max_rows, 1);
+    off = al(off + 2 * size_t(sp.part_rows) * sp.part_stride * 4, 128);
+    sp.off_seg = uint32_t(off);
+    const uint32_t rounds = (max_nnz + 31) / 32;
+    sp.seg_rounds = std::min<uint32_t>(rounds, 32);
+    off += 2 * size_t(sp.seg_rounds) * 128;
+    gseg_rounds = rounds - sp.seg_rounds;
+    sp.off_ring = uint32_t(al(off, 1024));
+    // big slots: a CTA's whole share of a 4096-column layer fits one chunk
+    sp.slot_bytes = uint32_t(al(std::max<uint32_t>(48 * 1024, max_rec), 128));
+    if (size_t(smax) < size_t(sp.off_ring) + 2 * size_t(sp.slot_bytes))
+        return fail(DSQ_E_UNSUPPORTED, "stack: layer too large for the shared-memory ring "
+                    "(x %u B, record %u B)", sp.x_bytes, max_rec);
+    sp.n_slots = std::min<uint32_t>((uint32_t(smax) - sp.off_ring) / sp.slot_bytes, 56);
+    sp.smem_bytes = sp.off_ring + sp.n_slots * sp.slot_bytes;
+    sp.grid = uint32_t(G);
+    sp.bits = bits;
+    for (uint32_t i = 0; i < n && i < kInlineLayers; ++i) fill_desc(sp.inl[i], Ls[i], sp.slot_bytes);
+    return DSQ_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// layer handle
+// ---------------------------------------------------------------------------
+struct dsq_cuda_layer {
+    int device = 0;
+    int num_sms = 0;
+    std::string name;
+    uint32_t rows = 0, cols = 0, bits = 0, groups = 1, nnz = 0, hybrid_top_k = 0;
+    uint32_t n_rb = 0, ng = 0, n_workers = 0, ctas = 0;
+    uint32_t luts_exact = 1, values_exact = 1;
+    uint64_t algorithmic_bytes = 0;
+    void* arena = nullptr;      // one device allocation for everything below
+    size_t arena_bytes = 0;
+    LayerParams P{};
+    WorkTable W{};
+    uint16_t* x16 = nullptr;    // fp16 staging of an fp32 x
+    float* y32 = nullptr;       // host-API output staging
+    float* x32 = nullptr;       // host-API input staging
+    uint16_t* dense_w = nullptr;  // lazily materialized fp16 dense W (reference kernel)
+    // row-record layout (bits 3/4): the persistent stack kernel's format
+    bool rec_layout = false;
+    uint32_t ngp = 0, rw = 0;
+    const uint32_t* rec = nullptr;
+    const uint32_t* zero_rp = nullptr;      // all-zero row_ptr (LUT-only products)
+    std::vector<uint32_t> row_ptr_host;
+    StackParams sp1{};                      // single-layer stack plan
+    uint32_t* stack_counters = nullptr;     // [2]
+    float* gseg1 = nullptr;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;       // guards dense_w materialization
+    std::mutex host_mu;  // serializes the host-buffer API on the internal stream
+};
+
+extern "C" {
+
+int dsq_cuda_abi_version(void) { return DSQ_CUDA_ABI_VERSION; }
+
+const char* dsq_cuda_last_error(void) { return g_err.c_str(); }
+
+uint64_t dsq_bytes_touched_estimate(uint32_t rows, uint32_t cols, uint32_t bits,
+                                    uint32_t group_size, uint64_t nnz) {
+    // packfmt.cpp:98-121 + kernels.cpp:205-212
+    const uint64_t weights = uint64_t(rows) * cols;
+    uint64_t total_bits;
+    if (bits == 16) {
+        total_bits = weights * 16;
+    } else {
+        const uint64_t gpr = group_size == 0 ? 1 : cols / group_size;
+        total_bits = uint64_t(rows) * ((uint64_t(cols) * bits + 7) / 8) * 8;
+        total_bits += uint64_t(rows) * gpr * (1u << bits) * 16;
+        if (nnz > 0) total_bits += nnz * 32 + (uint64_t(rows) + 1) * 32;
+    }
+    return total_bits / 8 + uint64_t(cols) * 2 + uint64_t(rows) * 2;
+}
+
+static int validate_view(const dsq_layer_view* v) {
+    if (!v) return fail(DSQ_E_INVALID_ARGUMENT, "null layer view");
+    if (!v->name || !v->name[0]) return fail(DSQ_E_INVALID_ARGUMENT, "layer: empty name");
+    const dsq_packed_view& p = v->packed;
+    // PackedDense::validate (packfmt.cpp:7-16)
+    if (p.bits < 1 || p.bits > 8)
+        return fail(DSQ_E_INVALID_ARGUMENT, "packed: bits must be in 1..8");
+    if (p.rows < 1 || p.cols < 1) return fail(DSQ_E_EMPTY_DIMENSION, "packed: empty dims");
+    if (p.groups_per_row < 1 || p.cols % p.groups_per_row != 0)
+        return fail(DSQ_E_SHAPE_MISMATCH, "packed: groups_per_row must divide cols");
+    if (!p.luts_f32 == !p.luts_f16)
+        return fail(DSQ_E_SHAPE_MISMATCH, "packed: exactly one of luts_f32/luts_f16 required");
+    if (!p.payload || p.payload_len != size_t(p.rows) * row_stride(p.cols, p.bits))
+        return fail(DSQ_E_SHAPE_MISMATCH, "packed: payload size mismatch");
+    // CsrMatrix::validate (dns.cpp:10-29)
+    const dsq_csr_view& s = v->sparse;
+    if (s.cols >= 65536u) return fail(DSQ_E_DIMENSION_OVERFLOW, "csr: cols must be < 65536");
+    if (!s.row_ptr) return fail(DSQ_E_SHAPE_MISMATCH, "csr: bad row_ptr length");
+    if (s.row_ptr[0] != 0) return fail(DSQ_E_INTERNAL, "csr: row_ptr[0] != 0");
+    for (uint32_t r = 0; r < s.rows; ++r) {
+        if (s.row_ptr[r] > s.row_ptr[r + 1])
+            return fail(DSQ_E_INTERNAL, "csr: row_ptr not nondecreasing");
+        for (uint32_t q = s.row_ptr[r]; q < s.row_ptr[r + 1]; ++q) {
+            if (q >= s.nnz) return fail(DSQ_E_SHAPE_MISMATCH, "csr: nnz mismatch");
+            if (s.col_idx[q] >= s.cols)
+                return fail(DSQ_E_INTERNAL, "csr: column index out of range");
+            if (q > s.row_ptr[r] && s.col_idx[q - 1] >= s.col_idx[q])
+                return fail(DSQ_E_INTERNAL, "csr: columns not strictly increasing");
+        }
+    }
+    if (s.row_ptr[s.rows] != s.nnz) return fail(DSQ_E_SHAPE_MISMATCH, "csr: nnz mismatch");
+    if (s.nnz > 0 && (!s.col_idx || (!s.values_f32 == !s.values_f16)))
+        return fail(DSQ_E_SHAPE_MISMATCH, "csr: exactly one of values_f32/values_f16 required");
+    for (uint32_t q = 0; q < s.nnz; ++q) {
+        const float f = s.values_f32 ? s.values_f32[q] : f16_to_f32(s.values_f16[q]);
+        if (!std::isfinite(f)) return fail(DSQ_E_NON_FINITE_VALUE, "csr: non-finite value");
+    }
+    // QuantizedLayer::validate (packfmt.cpp:82-92)
+    if (p.rows != v->rows || p.cols != v->cols)
+        return fail(DSQ_E_SHAPE_MISMATCH, "%s: packed dims mismatch", v->name);
+    if (s.rows != v->rows || s.cols != v->cols)
+        return fail(DSQ_E_SHAPE_MISMATCH, "%s: sparse dims mismatch", v->name);
+    if (p.groups_per_row != 1)
+        return fail(DSQ_E_UNSUPPORTED,
+                    "%s: device path implements channel-wise LUTs (groups_per_row == 1)", v->name);
+    return DSQ_OK;
+}
+
+int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** out) {
+    if (!out) return fail(DSQ_E_INVALID_ARGUMENT, "null output handle");
+    *out = nullptr;
+    int rc = validate_view(v);
+    if (rc) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(DSQ_E_NO_DEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(DSQ_E_NO_DEVICE, "bad device %d", device);
+    CUDA_TRY(cudaSetDevice(device));
+    int num_sms = 0;
+    if ((rc = query_num_sms(device, &num_sms))) return rc;
+
+    auto* L = new dsq_cuda_layer;
+    L->device = device;
+    L->num_sms = num_sms;
+    L->name = v->name;
+    L->rows = v->rows;
+    L->cols = v->cols;
+    L->bits = v->packed.bits;
+    L->nnz = v->sparse.nnz;
+    L->hybrid_top_k = v->hybrid_top_k;
+    const uint32_t bits = L->bits, rows = L->rows, cols = L->cols;
+    const uint32_t n_rb = ceil_div(rows, kRowBlock), ng = ceil_div(cols, kGroupCols);
+    const uint32_t K = 1u << bits;
+    L->n_rb = n_rb;
+    L->ng = ng;
+    L->algorithmic_bytes = dsq_bytes_touched_estimate(rows, cols, bits, 0, L->nnz);
+
+    // ---- LUT -> fp16 [n_rb*32][K]
+    std::vector<uint16_t> lut(size_t(n_rb) * kRowBlock * K, 0);
+    for (size_t i = 0; i < size_t(rows) * K; ++i) {
+        if (v->packed.luts_f16) {
+            lut[i] = v->packed.luts_f16[i];
+        } else {
+            const float f = v->packed.luts_f32[i];
+            lut[i] = f32_to_f16(f);
+            if (f16_to_f32(lut[i]) != f) L->luts_exact = 0;
+        }
+        const uint16_t h = lut[i];
+        if ((h & 0x7c00u) == 0x7c00u) {
+            delete L;
+            return fail(DSQ_E_NON_FINITE_VALUE,
+                        "%s: LUT centroid %zu is not finite in fp16", v->name, i);
+        }
+    }
+    const size_t stride = row_stride(cols, bits);
+    const bool rec_layout = (bits == 3 || bits == 4);
+    const uint32_t ngp = (ng + 3) & ~3u;
+    const uint32_t lw = bits == 3 ? 4 : 8;
+    const uint32_t rw = rec_layout ? lw + bits * ngp : 0;
+    const size_t unit_words = size_t(bits) * 32;
+    const size_t n_units = size_t(n_rb) * ng;
+    std::vector<uint32_t> words;
+    if (rec_layout) {
+        // ---- row records: [LUT byte planes][index words, k-major] (stack.hpp)
+        words.assign(size_t(rows) * rw, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t r = 0; r < int64_t(rows); ++r) {
+            uint8_t idx[32];
+            uint32_t w[8];
+            uint32_t* dst = words.data() + size_t(r) * rw;
+            const uint16_t* e = lut.data() + size_t(r) * K;
+            for (uint32_t set = 0; set < K / 8; ++set) {  // planes of entries 8*set .. 8*set+7
+                uint32_t l0 = 0, l1 = 0, h0 = 0, h1 = 0;
+                for (int i = 0; i < 4; ++i) {
+                    l0 |= uint32_t(e[8 * set + i] & 0xffu) << (8 * i);
+                    l1 |= uint32_t(e[8 * set + 4 + i] & 0xffu) << (8 * i);
+                    h0 |= uint32_t(e[8 * set + i] >> 8) << (8 * i);
+                    h1 |= uint32_t(e[8 * set + 4 + i] >> 8) << (8 * i);
+                }
+                dst[4 * set + 0] = l0;
+                dst[4 * set + 1] = l1;
+                dst[4 * set + 2] = h0;
+                dst[4 * set + 3] = h1;
+            }
+            const uint8_t* row = v->packed.payload + size_t(r) * stride;
+            for (uint32_t g = 0; g < ng; ++g) {
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t c = g * kGroupCols + j;
+                    idx[j] = c < cols ? uint8_t(ref_index(row, stride, c, bits)) : 0;
+                }
+                encode_unit(idx, bits, w);
+                for (uint32_t k = 0; k < bits; ++k) dst[lw + g * bits + k] = w[k];
+            }
+        }
+    } else {
+        // ---- tiled index words (generic widths, stream-K kernel)
+        words.assign(n_units * unit_words, 0);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t rb = 0; rb < int64_t(n_rb); ++rb) {
+            uint8_t idx[32];
+            uint32_t w[8];
+            for (uint32_t lane = 0; lane < kRowBlock; ++lane) {
+                const uint32_t r = uint32_t(rb) * kRowBlock + lane;
+                const uint8_t* row = r < rows ? v->packed.payload + size_t(r) * stride : nullptr;
+                for (uint32_t g = 0; g < ng; ++g) {
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t c = g * kGroupCols + j;
+                        idx[j] = (row && c < cols) ? uint8_t(ref_index(row, stride, c, bits)) : 0;
+                    }
+                    encode_unit(idx, bits, w);
+                    uint32_t* dst = words.data() + (size_t(rb) * ng + g) * unit_words;
+                    for (uint32_t k = 0; k < bits; ++k) dst[k * 32 + lane] = w[k];
+                }
+            }
+        }
+    }
+    L->rec_layout = rec_layout;
+    L->ngp = ngp;
+    L->rw = rw;
+    L->row_ptr_host.assign(v->sparse.row_ptr, v->sparse.row_ptr + rows + 1);
+    // ---- CSR entries: col | fp16(delta) << 16
+    std::vector<uint32_t> csr(std::max<uint32_t>(L->nnz, 1), 0);
+    for (uint32_t q = 0; q < L->nnz; ++q) {
+        uint16_t h;
+        if (v->sparse.values_f16) {
+            h = v->sparse.values_f16[q];
+        } else {
+            const float f = v->sparse.values_f32[q];
+            h = f32_to_f16(f);
+            if (f16_to_f32(h) != f) L->values_exact = 0;
+        }
+        if ((h & 0x7c00u) == 0x7c00u) {
+            delete L;
+            return fail(DSQ_E_NON_FINITE_VALUE, "%s: CSR delta %u is not finite in fp16",
+                        v->name, q);
+        }
+        csr[q] = uint32_t(v->sparse.col_idx[q]) | (uint32_t(h) << 16);
+    }
+    // ---- balanced schedule (stream-K over units, CSR cost weighted by nnz)
+    const double beta = 1.0 / 64.0;  // one CSR entry ~ 1/64 of a 32x32 dense unit
+    std::vector<double> rb_cost(n_rb);
+    for (uint32_t rb = 0; rb < n_rb; ++rb) {
+        const uint32_t r0 = std::min(rb * kRowBlock, rows), r1 = std::min(r0 + kRowBlock, rows);
+        const double nz = double(v->sparse.row_ptr[r1] - v->sparse.row_ptr[r0]);
+        rb_cost[rb] = 1.0 + beta * nz / ng;  // per unit of this row block
+    }
+    double total = 0;
+    for (uint32_t rb = 0; rb < n_rb; ++rb) total += rb_cost[rb] * ng;
+    int ctas_per_sm = kCtasPerSmDefault;
+    if (const char* e = std::getenv("DSQ_CTAS_PER_SM")) ctas_per_sm = std::max(1, std::min(3, atoi(e)));
+    const uint32_t max_workers =
+        std::min<uint32_t>(uint32_t(num_sms) * ctas_per_sm * kWarpsPerCta, kMaxWorkers);
+    uint32_t nw = uint32_t(std::max<size_t>(1, std::min<size_t>(max_workers, (n_units + 1) / 2)));
+    std::vector<uint32_t> bounds;  // unit boundaries, nw+1 entries
+    bounds.reserve(nw + 1);
+    {
+        bounds.push_back(0);
+        double acc = 0;
+        uint32_t w = 1;
+        for (size_t u = 0; u < n_units && w < nw; ++u) {
+            acc += rb_cost[u / ng];
+            while (w < nw && acc >= total * double(w) / nw - 1e-9) {
+                bounds.push_back(uint32_t(u + 1));
+                ++w;
+            }
+        }
+        while (bounds.size() < size_t(nw) + 1) bounds.push_back(uint32_t(n_units));
+        bounds.back() = uint32_t(n_units);
+    }
+    // drop empty ranges -> strictly increasing u0[]
+    {
+        uint32_t n = 0;
+        L->W.u0[0] = 0;
+        for (uint32_t w = 0; w < nw; ++w)
+            if (bounds[w + 1] > bounds[w]) L->W.u0[++n] = bounds[w + 1];
+        nw = n;
+        L->W.n = nw;
+    }
+    {
+        L->n_workers = nw;
+        L->ctas = ceil_div(nw, kWarpsPerCta);
+        const size_t scratch_floats = size_t(2) * nw * kRowBlock;
+        // ---- one arena
+        auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t o_words = 0;
+        const size_t o_lut = o_words + al(words.size() * 4);
+        const size_t o_rowptr = o_lut + al(lut.size() * 2);
+        const size_t o_csr = o_rowptr + al((size_t(rows) + 1) * 4);
+        const size_t o_scratch = o_csr + al(csr.size() * 4);
+        const size_t o_counters = o_scratch + al(scratch_floats * 4);
+        const size_t o_x16 = o_counters + al(size_t(n_rb) * 4);
+        const size_t o_x32 = o_x16 + al((size_t(ng) * kGroupCols + 8) * 2);
+        const size_t o_y32 = o_x32 + al(size_t(cols) * 4);
+        const size_t o_zrp = o_y32 + al(size_t(rows) * 4);
+        const size_t o_scnt = o_zrp + al((size_t(rows) + 1) * 4);
+        // single-layer stack plan (bits 3/4)
+        uint32_t gseg_rounds = 0;
+        if (rec_layout) {
+            StackPlanLayer pl{rows, cols, ng, ngp, rw, max_nnz_per_cta(L->row_ptr_host, rows, num_sms)};
+            int prc = plan_stack(&pl, 1, num_sms, bits, L->sp1, gseg_rounds);
+            if (prc) {
+                delete L;
+                return prc;
+            }
+        }
+        const size_t o_gseg = o_scnt + al(2 * 4);
+        const size_t total_bytes = o_gseg + al(size_t(num_sms) * 2 * gseg_rounds * 32 * 4 + 4);
+        cudaError_t e = cudaMalloc(&L->arena, total_bytes);
+        if (e != cudaSuccess) {
+            delete L;
+            return cuda_fail(e, "cudaMalloc(layer arena)");
+        }
+        L->arena_bytes = total_bytes;
+        uint8_t* base = static_cast<uint8_t*>(L->arena);
+        LayerParams& P = L->P;
+        P.words = reinterpret_cast<const uint32_t*>(base + o_words);
+        P.lut = reinterpret_cast<const uint16_t*>(base + o_lut);
+        P.row_ptr = reinterpret_cast<const uint32_t*>(base + o_rowptr);
+        P.csr = reinterpret_cast<const uint32_t*>(base + o_csr);
+        P.scratch = reinterpret_cast<float*>(base + o_scratch);
+        P.counters = reinterpret_cast<uint32_t*>(base + o_counters);
+        P.rows = rows;
+        P.cols = cols;
+        P.bits = bits;
+        P.n_rb = n_rb;
+        P.ng = ng;
+        P.n_workers = nw;
+        P.nnz = L->nnz;
+        L->x16 = reinterpret_cast<uint16_t*>(base + o_x16);
+        L->x32 = reinterpret_cast<float*>(base + o_x32);
+        L->y32 = reinterpret_cast<float*>(base + o_y32);
+        L->zero_rp = reinterpret_cast<const uint32_t*>(base + o_zrp);
+        L->stack_counters = reinterpret_cast<uint32_t*>(base + o_scnt);
+        L->gseg1 = reinterpret_cast<float*>(base + o_gseg);
+        if (rec_layout) {
+            L->rec = reinterpret_cast<const uint32_t*>(base + o_words);
+            StackParams& sp = L->sp1;
+            sp.counters = L->stack_counters;
+            sp.gseg = L->gseg1;
+            sp.gseg_rounds = gseg_rounds;
+            StackLayerDesc& d = sp.inl[0];
+            d.rec = L->rec;
+            d.row_ptr = P.row_ptr;
+            d.csr = P.csr;
+        }
+        auto up = [&](size_t off, const void* src, size_t n) {
+            return cudaMemcpy(base + off, src, n, cudaMemcpyHostToDevice);
+        };
+        if ((e = up(o_words, words.data(), words.size() * 4)) != cudaSuccess ||
+            (e = up(o_lut, lut.data(), lut.size() * 2)) != cudaSuccess ||
+            (e = up(o_rowptr, v->sparse.row_ptr, (size_t(rows) + 1) * 4)) != cudaSuccess ||
+            (e = up(o_csr, csr.data(), csr.size() * 4)) != cudaSuccess ||
+            (e = cudaMemset(base + o_counters, 0, size_t(n_rb) * 4)) != cudaSuccess ||
+            (e = cudaMemset(base + o_zrp, 0, (size_t(rows) + 1) * 4)) != cudaSuccess ||
+            (e = cudaMemset(base + o_scnt, 0, 2 * 4)) != cudaSuccess ||
+            (e = cudaMemset(base + o_x16, 0, (size_t(ng) * kGroupCols + 8) * 2)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            cudaFree(L->arena);
+            delete L;
+            return cuda_fail(e, "layer upload");
+        }
+    }
+    *out = L;
+    return DSQ_OK;
+}
+
+int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
+    if (!L) return DSQ_OK;
+    cudaSetDevice(L->device);
+    if (L->stream) cudaStreamDestroy(L->stream);
+    if (L->dense_w) cudaFree(L->dense_w);
+    if (L->arena) cudaFree(L->arena);
+    delete L;
+    return DSQ_OK;
+}
+
+int dsq_cuda_layer_get_info(const dsq_cuda_layer* L, dsq_layer_info* info) {
+    if (!L || !info) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    info->rows = L->rows;
+    info->cols = L->cols;
+    info->bits = L->bits;
+    info->groups_per_row = 1;
+    info->nnz = L->nnz;
+    info->device_bytes = L->arena_bytes + (L->dense_w ? size_t(L->rows) * L->cols * 2 : 0);
+    info->algorithmic_bytes = L->algorithmic_bytes;
+    info->luts_exact_f16 = L->luts_exact;
+    info->values_exact_f16 = L->values_exact;
+    info->workers = L->n_workers;
+    info->ctas = L->ctas;
+    return DSQ_OK;
+}
+
+static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(L->mu);
+    if (L->dense_w) return DSQ_OK;
+    CUDA_TRY(cudaMalloc(&L->dense_w, size_t(L->rows) * L->cols * 2));
+    if (L->rec_layout)
+        CUDA_TRY(launch_decode_records(1, L->bits, L->rec, L->rows, L->cols, L->ng, L->ngp,
+                                       L->rw, L->dense_w, st));
+    else
+        CUDA_TRY(launch_decode(1, L->P, L->dense_w, st));
+    return DSQ_OK;
+}
+
+static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_dtype, void* y,
+                     int y_dtype, uint32_t batch, cudaStream_t st, bool pdl) {
+    auto* L = const_cast<dsq_cuda_layer*>(Lc);
+    if (!L || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (batch != 1) return fail(DSQ_E_UNSUPPORTED, "batch must be 1 (ABI v1)");
+    if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)
+        return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);
+    if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
+        return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
+    const uint16_t* x16;
+    if (x_dtype == DSQ_F32) {
+        CUDA_TRY(launch_f32_to_f16(static_cast<const float*>(x), L->x16, L->cols, st, pdl));
+        x16 = L->x16;
+    } else if (x_dtype == DSQ_F16) {
+        if (reinterpret_cast<uintptr_t>(x) & 15u)
+            return fail(DSQ_E_INVALID_ARGUMENT, "fp16 x must be 16-byte aligned");
+        x16 = static_cast<const uint16_t*>(x);
+    } else {
+        return fail(DSQ_E_INVALID_ARGUMENT, "x dtype must be F32 or F16");
+    }
+    const bool yh = y_dtype == DSQ_F16;
+    if (kernel == DSQ_KERNEL_REFERENCE) {
+        int rc = ensure_dense(L, st);
+        if (rc) return rc;
+        CUDA_TRY(launch_dense(L->dense_w, L->rows, L->cols, x16, y, yh, L->num_sms, st, pdl));
+        return DSQ_OK;
+    }
+    const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
+    if (L->rec_layout && mode != 1) {
+        // K7 persistent kernel, one layer carried inline in the launch params
+        StackParams sp = L->sp1;
+        StackLayerDesc& d = sp.inl[0];
+        d.x = x16;
+        d.y = y;
+        d.y_f16 = yh ? 1u : 0u;
+        if (mode == 0) d.row_ptr = L->zero_rp;  // LUT part only: empty CSR
+        sp.n_layers = 1;
+        sp.layers = nullptr;
+        CUDA_TRY(launch_stack(sp, st, pdl));
+        return DSQ_OK;
+    }
+    CUDA_TRY(launch_fused(mode, L->P, L->W, x16, y, yh, L->ctas, st, pdl));
+    return DSQ_OK;
+}
+
+int dsq_cuda_gemv(const dsq_cuda_layer* L, int kernel, const void* x, int x_dtype, void* y,
+                  int y_dtype, uint32_t batch, void* stream) {
+    if (L) cudaSetDevice(L->device);
+    return gemv_impl(L, kernel, x, x_dtype, y, y_dtype, batch, static_cast<cudaStream_t>(stream),
+                     true);
+}
+
+int dsq_cuda_lut_gemv(const dsq_cuda_layer* L, const void* x, int xd, void* y, int yd,
+                      uint32_t batch, void* stream) {
+    return dsq_cuda_gemv(L, DSQ_KERNEL_LUT, x, xd, y, yd, batch, stream);
+}
+int dsq_cuda_csr_gemv(const dsq_cuda_layer* L, const void* x, int xd, void* y, int yd,
+                      uint32_t batch, void* stream) {
+    return dsq_cuda_gemv(L, DSQ_KERNEL_CSR, x, xd, y, yd, batch, stream);
+}
+int dsq_cuda_fused_gemv(const dsq_cuda_layer* L, const void* x, int xd, void* y, int yd,
+                        uint32_t batch, void* stream) {
+    return dsq_cuda_gemv(L, DSQ_KERNEL_FUSED, x, xd, y, yd, batch, stream);
+}
+
+int dsq_cuda_dense_gemv(const uint16_t* w, uint32_t rows, uint32_t cols, const void* x,
+                        int x_dtype, void* y, int y_dtype, void* stream) {
+    if (!w || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (rows < 1 || cols < 1) return fail(DSQ_E_EMPTY_DIMENSION, "dense: empty dims");
+    if (x_dtype != DSQ_F16) return fail(DSQ_E_INVALID_ARGUMENT, "dense: x must be F16");
+    if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
+        return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    int rc = query_num_sms(dev, &sms);
+    if (rc) return rc;
+    CUDA_TRY(launch_dense(w, rows, cols, static_cast<const uint16_t*>(x), y, y_dtype == DSQ_F16,
+                          sms, static_cast<cudaStream_t>(stream), true));
+    return DSQ_OK;
+}
+
+int dsq_cuda_matvec_host(const dsq_cuda_layer* Lc, int kernel, const float* x_host,
+                         double* y_host) {
+    auto* L = const_cast<dsq_cuda_layer*>(Lc);
+    if (!L || !x_host || !y_host) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(L->device);
+    std::lock_guard<std::mutex> lk(L->host_mu);
+    CUDA_TRY(cudaMemcpyAsync(L->x32, x_host, size_t(L->cols) * 4, cudaMemcpyHostToDevice,
+                             L->stream));
+    int rc = gemv_impl(L, kernel, L->x32, DSQ_F32, L->y32, DSQ_F32, 1, L->stream, false);
+    if (rc) return rc;
+    std::vector<float> y(L->rows);
+    CUDA_TRY(cudaMemcpyAsync(y.data(), L->y32, size_t(L->rows) * 4, cudaMemcpyDeviceToHost,
+                             L->stream));
+    CUDA_TRY(cudaStreamSynchronize(L->stream));
+    for (uint32_t r = 0; r < L->rows; ++r) y_host[r] = double(y[r]);
+    return DSQ_OK;
+}
+
+int dsq_cuda_unpack(const dsq_cuda_layer* L, uint16_t* assign_dev, void* stream) {
+    if (!L || !assign_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(L->device);
+    if (L->rec_layout)
+        CUDA_TRY(launch_decode_records(0, L->bits, L->rec, L->rows, L->cols, L->ng, L->ngp,
+                                       L->rw, assign_dev, static_cast<cudaStream_t>(stream)));
+    else
+        CUDA_TRY(launch_decode(0, L->P, assign_dev, static_cast<cudaStream_t>(stream)));
+    return DSQ_OK;
+}
+
+int dsq_cuda_dequant(const dsq_cuda_layer* L, void* w_dev, int out_dtype, void* stream) {
+    if (!L || !w_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (out_dtype != DSQ_F16 && out_dtype != DSQ_F32)
+        return fail(DSQ_E_INVALID_ARGUMENT, "dequant: out dtype must be F16 or F32");
+    cudaSetDevice(L->device);
+    const int mode = out_dtype == DSQ_F16 ? 1 : 2;
+    if (L->rec_layout)
+        CUDA_TRY(launch_decode_records(mode, L->bits, L->rec, L->rows, L->cols, L->ng, L->ngp,
+                                       L->rw, w_dev, static_cast<cudaStream_t>(stream)));
+    else
+        CUDA_TRY(launch_decode(mode, L->P, w_dev, static_cast<cudaStream_t>(stream)));
+    return DSQ_OK;
+}
+
+struct dsq_cuda_stack {
+    int device = 0;
+    uint32_t n = 0;
+    StackParams sp{};
+    void* arena = nullptr;
+    unsigned long long* trace = nullptr;  // DSQ_STACK_TRACE=1: per-CTA layer timeline
+};
+
+int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                          const void* const* xs, void* const* ys, int y_dtype,
+                          dsq_cuda_stack** out) {
+    if (!out || !layers || !deps || !xs || !ys || n == 0)
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack: null argument or empty stack");
+    *out = nullptr;
+    if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack: y dtype must be F32 or F16");
+    const dsq_cuda_layer* L0 = layers[0];
+    if (!L0) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null layer");
+    std::vector<StackPlanLayer> pl(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        const dsq_cuda_layer* L = layers[i];
+        if (!L) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null layer %u", i);
+        if (!L->rec_layout || L->bits != L0->bits)
+            return fail(DSQ_E_UNSUPPORTED, "stack: layers must all be 3-bit or all 4-bit");
+        if (L->device != L0->device)
+            return fail(DSQ_E_INVALID_ARGUMENT, "stack: layers on different devices");
+        if (deps[i] >= 0) {
+            if (uint32_t(deps[i]) >= i)
+                return fail(DSQ_E_INVALID_ARGUMENT, "stack: deps[%u] must precede it", i);
+            if (layers[deps[i]]->rows != L->cols)
+                return fail(DSQ_E_SHAPE_MISMATCH, "stack: layer %u cols != rows of its input", i);
+            if (y_dtype != DSQ_F16)
+                return fail(DSQ_E_INVALID_ARGUMENT, "stack: chained layers need F16 outputs");
+        } else if (!xs[i] || (reinterpret_cast<uintptr_t>(xs[i]) & 15u)) {
+            return fail(DSQ_E_INVALID_ARGUMENT, "stack: x %u must be a 16-byte aligned fp16 buffer", i);
+        }
+        if (!ys[i]) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null y %u", i);
+        pl[i] = StackPlanLayer{L->rows, L->cols, L->ng, L->ngp, L->rw,
+                               max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
+    }
+    CUDA_TRY(cudaSetDevice(L0->device));
+    auto* S = new dsq_cuda_stack;
+    S->device = L0->device;
+    S->n = n;
+    uint32_t gseg_rounds = 0;
+    int rc = plan_stack(pl.data(), n, L0->num_sms, L0->bits, S->sp, gseg_rounds);
+    if (rc) {
+        delete S;
+        return rc;
+    }
+    std::vector<StackLayerDesc> descs(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        StackLayerDesc& d = descs[i];
+        fill_desc(d, pl[i], S->sp.slot_bytes);
+        const dsq_cuda_layer* L = layers[i];
+        d.rec = L->rec;
+        d.row_ptr = L->P.row_ptr;
+        d.csr = L->P.csr;
+        d.dep = deps[i] >= 0 ? uint32_t(deps[i]) : kNoDep;
+        d.x = deps[i] >= 0 ? static_cast<const uint16_t*>(ys[deps[i]])
+                           : static_cast<const uint16_t*>(xs[i]);
+        d.y = ys[i];
+        d.y_f16 = y_dtype == DSQ_F16 ? 1u : 0u;
+        if (i < kInlineLayers) S->sp.inl[i] = d;
+    }
+    const size_t tb = (size_t(n) * sizeof(StackLayerDesc) + 255) & ~size_t(255);
+    const size_t cb = ((size_t(n) + 1) * 4 + 255) & ~size_t(255);
+    const size_t gb = size_t(L0->num_sms) * 2 * gseg_rounds * 32 * 4 + 4;
+    cudaError_t e = cudaMalloc(&S->arena, tb + cb + gb);
+    if (e != cudaSuccess) {
+        delete S;
+        return cuda_fail(e, "cudaMalloc(stack)");
+    }
+    uint8_t* base = static_cast<uint8_t*>(S->arena);
+    if ((e = cudaMemcpy(base, descs.data(), n * sizeof(StackLayerDesc), cudaMemcpyHostToDevice)) !=
+            cudaSuccess ||
+        (e = cudaMemset(base + tb, 0, cb)) != cudaSuccess) {
+        cudaFree(S->arena);
+        delete S;
+        return cuda_fail(e, "stack upload");
+    }
+    S->sp.layers = reinterpret_cast<const StackLayerDesc*>(base);
+    S->sp.counters = reinterpret_cast<uint32_t*>(base + tb);
+    S->sp.gseg = reinterpret_cast<float*>(base + tb + cb);
+    S->sp.gseg_rounds = gseg_rounds;
+    S->sp.n_layers = n;
+    S->sp.trace = nullptr;
+    if (const char* t = std::getenv("DSQ_STACK_TRACE")) {
+        if (t[0] == '1') {
+            const size_t tbytes = size_t(S->sp.grid) * n * kTrSlots * 8;
+            if (cudaMalloc(&S->trace, tbytes) == cudaSuccess) {
+                cudaMemset(S->trace, 0, tbytes);
+                S->sp.trace = S->trace;
+            }
+        }
+    }
+    *out = S;
+    return DSQ_OK;
+}
+
+// debug: copy the stack timeline (grid * n * kTrSlots u64) to host; returns
+// the number of u64 written (0 if tracing is off)
+extern "C" uint64_t dsq_cuda_stack_trace(dsq_cuda_stack* S, unsigned long long* host,
+                                         uint64_t cap) {
+    if (!S || !S->trace) return 0;
+    const uint64_t n = uint64_t(S->sp.grid) * S->n * kTrSlots;
+    if (cap < n) return 0;
+    cudaSetDevice(S->device);
+    cudaMemcpy(host, S->trace, n * 8, cudaMemcpyDeviceToHost);
+    return n;
+}
+
+int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
+    if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
+    cudaSetDevice(S->device);
+    CUDA_TRY(launch_stack(S->sp, static_cast<cudaStream_t>(stream), true));
+    return DSQ_OK;
+}
+
+int dsq_cuda_stack_destroy(dsq_cuda_stack* S) {
+    if (!S) return DSQ_OK;
+    cudaSetDevice(S->device);
+    if (S->arena) cudaFree(S->arena);
+    if (S->trace) cudaFree(S->trace);
+    delete S;
+    return DSQ_OK;
+}
+
+int dsq_cuda_gemv_many(dsq_cuda_layer* const* layers, uint32_t n, int kernel,
+                       const void* const* xs, int x_dtype, void* const* ys, int y_dtype,
+                       void* stream) {
+    if (!layers || !xs || !ys) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    for (uint32_t i = 0; i < n; ++i) {
+        int rc = gemv_impl(layers[i], kernel, xs[i], x_dtype, ys[i], y_dtype, 1,
+                           static_cast<cudaStream_t>(stream), true);
+        if (rc) return rc;
+    }
+    return DSQ_OK;
+}
+
+}  // extern "C"
