@@ -180,7 +180,9 @@ uint32_t max_nnz_per_cta(const std::vector<uint32_t>& rp, uint32_t rows, int G) 
     return m;
 }
 
-void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes) {
+void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, int G) {
+    d.rq = l.rows / uint32_t(G);
+    d.rr = l.rows % uint32_t(G);
     d.rows = l.rows;
     d.cols = l.cols;
     d.ng = l.ng;
@@ -189,6 +191,8 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes) 
     d.chunk_rows = std::max<uint32_t>(1, slot_bytes / (l.rw * 4));
     d.nslices = ceil_div(l.ng, 32);
     d.dep = kNoDep;
+    d.nch_lo = ceil_div(d.rq, d.chunk_rows);
+    d.nch_hi = ceil_div(d.rq + 1, d.chunk_rows);
 }
 
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
@@ -234,7 +238,12 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.smem_bytes = sp.off_ring + sp.n_slots * sp.slot_bytes;
     sp.grid = uint32_t(G);
     sp.bits = bits;
-    for (uint32_t i = 0; i < n && i < kInlineLayers; ++i) fill_desc(sp.inl[i], Ls[i], sp.slot_bytes);
+    sp.consumers = kStackConsumersDefault;
+    if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
+        const int c = atoi(e);
+        if (c == 8 || c == 16 || c == 24) sp.consumers = uint32_t(c);
+    }
+    for (uint32_t i = 0; i < n && i < kInlineLayers; ++i) fill_desc(sp.inl[i], Ls[i], sp.slot_bytes, G);
     return DSQ_OK;
 }
 
@@ -816,7 +825,7 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
     std::vector<StackLayerDesc> descs(n);
     for (uint32_t i = 0; i < n; ++i) {
         StackLayerDesc& d = descs[i];
-        fill_desc(d, pl[i], S->sp.slot_bytes);
+        fill_desc(d, pl[i], S->sp.slot_bytes, L0->num_sms);
         const dsq_cuda_layer* L = layers[i];
         d.rec = L->rec;
         d.row_ptr = L->P.row_ptr;

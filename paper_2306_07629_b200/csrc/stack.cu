@@ -43,10 +43,6 @@
 
 namespace sqz {
 
-__device__ __forceinline__ uint32_t split_rows(uint32_t rows, uint32_t cta, uint32_t G) {
-    return uint32_t((uint64_t(rows) * cta) / G);
-}
-
 __device__ __forceinline__ const StackLayerDesc& layer_desc(const StackParams& p, uint32_t l) {
     return l < kInlineLayers && p.n_layers <= kInlineLayers ? p.inl[l] : p.layers[l];
 }
@@ -69,35 +65,78 @@ __device__ __forceinline__ float reduce4(float v0, float v1, float v2, float v3,
     return k;
 }
 
+// Operands of one (row, 32-group slice) for one lane: LUT planes + words.
 template <int BITS>
-__device__ __forceinline__ float row_slice_dot(const uint32_t* rec, uint32_t g,
-                                               const uint4 (&xv)[4]) {
+struct RowOps {
+    uint4 pl[BITS == 3 ? 1 : 2];
+    uint32_t w[BITS];
+};
+
+template <int BITS>
+__device__ __forceinline__ void load_row(const uint32_t* rec, uint32_t g, bool on, RowOps<BITS>& o) {
+    if constexpr (BITS == 3) {
+        o.pl[0] = on ? *reinterpret_cast<const uint4*>(rec) : make_uint4(0, 0, 0, 0);
+        const uint32_t* w = rec + 4 + 3 * g;
+        o.w[0] = on ? w[0] : 0u;
+        o.w[1] = on ? w[1] : 0u;
+        o.w[2] = on ? w[2] : 0u;
+    } else {
+        o.pl[0] = on ? *reinterpret_cast<const uint4*>(rec) : make_uint4(0, 0, 0, 0);
+        o.pl[1] = on ? *reinterpret_cast<const uint4*>(rec + 4) : make_uint4(0, 0, 0, 0);
+        const uint4 w4 = on ? *reinterpret_cast<const uint4*>(rec + 8 + 4 * g) : make_uint4(0, 0, 0, 0);
+        o.w[0] = w4.x;
+        o.w[1] = w4.y;
+        o.w[2] = w4.z;
+        o.w[3] = w4.w;
+    }
+}
+
+// zero operands decode to LUT entries 0.0 -> contribute exactly 0
+template <int BITS>
+__device__ __forceinline__ float row_dot(const RowOps<BITS>& o, const uint4 (&xv)[4]) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     if constexpr (BITS == 3) {
-        const uint4 q = *reinterpret_cast<const uint4*>(rec);
-        const Planes8 P{q.x, q.y, q.z, q.w};
-        const uint32_t* w = rec + 4 + 3 * g;
-        unit3(w[0], w[1], w[2], P, xv, a0, a1, a2, a3);
+        const Planes8 P{o.pl[0].x, o.pl[0].y, o.pl[0].z, o.pl[0].w};
+        unit3(o.w[0], o.w[1], o.w[2], P, xv, a0, a1, a2, a3);
     } else {
-        const uint4 q0 = *reinterpret_cast<const uint4*>(rec);
-        const uint4 q1 = *reinterpret_cast<const uint4*>(rec + 4);
         Planes16 P;
-        P.a = Planes8{q0.x, q0.y, q0.z, q0.w};
-        P.b = Planes8{q1.x, q1.y, q1.z, q1.w};
-        const uint4 w4 = *reinterpret_cast<const uint4*>(rec + 8 + 4 * g);
-        const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+        P.a = Planes8{o.pl[0].x, o.pl[0].y, o.pl[0].z, o.pl[0].w};
+        P.b = Planes8{o.pl[1].x, o.pl[1].y, o.pl[1].z, o.pl[1].w};
+        const uint32_t ww[4] = {o.w[0], o.w[1], o.w[2], o.w[3]};
         unit4(ww, P, xv, a0, a1, a2, a3);
     }
     return (a0 + a1) + (a2 + a3);
 }
 
-// Rows of a CTA's layer share are split into ceil(n / max_rows) near-equal
-// ring chunks (identical on producer and consumer side).
-__device__ __forceinline__ uint32_t chunk_count(uint32_t nrows, uint32_t max_rows) {
-    return (nrows + max_rows - 1) / max_rows;
+// CTA row share from the host-precomputed quotient/remainder (no division)
+struct Share {
+    uint32_t r0, n, nch;
+};
+__device__ __forceinline__ Share cta_share(const StackLayerDesc& d, uint32_t cta) {
+    Share s;
+    const bool hi = cta < d.rr;
+    s.r0 = cta * d.rq + (hi ? cta : d.rr);
+    s.n = d.rq + (hi ? 1u : 0u);
+    s.nch = hi ? d.nch_hi : d.nch_lo;
+    return s;
 }
-__device__ __forceinline__ uint32_t chunk_start(uint32_t nrows, uint32_t nch, uint32_t c) {
-    return uint32_t((uint64_t(nrows) * c) / nch);
+
+// 2-value butterfly: lane 0 -> row 0 total, lane 16 -> row 1 total
+__device__ __forceinline__ float reduce2(float v0, float v1, uint32_t lane) {
+    const bool hi = lane & 16;
+    float k = hi ? v1 : v0;
+    const float s = hi ? v0 : v1;
+    k += __shfl_xor_sync(0xffffffffu, s, 16);
+    k += __shfl_xor_sync(0xffffffffu, k, 8);
+    k += __shfl_xor_sync(0xffffffffu, k, 4);
+    k += __shfl_xor_sync(0xffffffffu, k, 2);
+    k += __shfl_xor_sync(0xffffffffu, k, 1);
+    return k;
+}
+__device__ __forceinline__ float reduce1(float v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
 }
 
 // warp-cooperative global -> shared copy with 8 loads in flight per lane
@@ -129,8 +168,46 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
             gtimer_ns();                                                                   \
     } while (0)
 
-template <int BITS>
-__global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_constant__ StackParams p) {
+// CSR deltas of the CTA's rows: 32-entry rounds j = first, first+stride, ...
+// of the CTA's contiguous entry slice; a lane starts a segment where a row
+// starts (row starts found in parallel: each lane tests <= ceil(nrows/32) row
+// pointers), then a segmented inclusive warp scan; round results go to segs.
+__device__ __forceinline__ void csr_rounds(const uint32_t* rp, uint32_t nrows, const uint32_t* ent,
+                                           const uint16_t* xh, float* segs, float* gseg,
+                                           uint32_t seg_rounds, uint32_t first, uint32_t stride,
+                                           uint32_t lane) {
+    const uint32_t e0 = rp[0], nz = rp[nrows] - e0;
+    const uint32_t rounds = (nz + 31) / 32;
+    for (uint32_t j = first; j < rounds; j += stride) {
+        const uint32_t base = e0 + j * 32;
+        const uint32_t pi = j * 32 + lane;
+        float prod = 0.f;
+        if (pi < nz) {
+            const uint32_t e = ent[pi];
+            prod = fma_h(uint16_t(e >> 16), xh[e & 0xffffu], 0.f);
+        }
+        uint32_t mybits = 0;
+        for (uint32_t r = lane; r < nrows; r += 32) {
+            const uint32_t a = rp[r];
+            if (a >= base && a < base + 32 && a < rp[r + 1]) mybits |= 1u << (a - base);
+        }
+        const uint32_t heads = __reduce_or_sync(0xffffffffu, mybits);
+        const uint32_t upto = heads & (0xffffffffu >> (31 - lane));
+        const uint32_t seg0 = upto ? (31u - __clz(upto)) : 0u;
+        float v = prod;
+#pragma unroll
+        for (uint32_t off = 1; off < 32; off <<= 1) {
+            const float t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= seg0 + off) v += t;
+        }
+        float* dst = j < seg_rounds ? segs + j * 32 : gseg + (j - seg_rounds) * 32;
+        dst[lane] = v;
+    }
+}
+
+template <int BITS, int NC>
+__global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_constant__ StackParams p) {
+    constexpr int kStackConsumers = NC;
     extern __shared__ __align__(1024) uint8_t sm[];
     // mbarriers: ring full/empty, then per buffer parity b in {0,1}
     uint64_t* full = reinterpret_cast<uint64_t*>(sm);
@@ -160,7 +237,10 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
     }
     __syncthreads();
 
-    if (warp == 0) {
+    // Warp roles.  The issue arbiter favours the highest warp id, so the
+    // latency-critical control warps take the top ids: consumers 0..NC-1,
+    // producer NC, loader NC+1, finisher NC+2.
+    if (warp == NC) {
         // ---------------- producer: weights only, never waits on x ----------
         pdl_trigger();
         if (lane == 0) {
@@ -168,13 +248,12 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
             uint32_t slot = 0, phase = 0;
             for (uint32_t l = 0; l < p.n_layers; ++l) {
                 const StackLayerDesc& d = layer_desc(p, l);
-                const uint32_t rows = d.rows, rw = d.rw;
+                const uint32_t rw = d.rw, cr = d.chunk_rows;
                 const uint32_t* rec = d.rec;
-                const uint32_t r0 = split_rows(rows, cta, G), r1 = split_rows(rows, cta + 1, G);
-                const uint32_t nch = chunk_count(r1 - r0, d.chunk_rows);
-                for (uint32_t c = 0; c < nch; ++c) {
-                    const uint32_t r = r0 + chunk_start(r1 - r0, nch, c);
-                    const uint32_t n = r0 + chunk_start(r1 - r0, nch, c + 1) - r;
+                const Share sh = cta_share(d, cta);
+                for (uint32_t c = 0; c < sh.nch; ++c) {
+                    const uint32_t r = sh.r0 + c * cr;
+                    const uint32_t n = min(cr, sh.n - c * cr);
                     const uint32_t bytes = n * rw * 4;
                     mbar_wait(&empty[slot], phase ^ 1u);
                     if (c == 0) DSQ_TRACE(l, kTrProdFirst);
@@ -191,7 +270,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
         return;
     }
 
-    if (warp == 1) {
+    if (warp == NC + 1) {
         // ---------------- loader: CSR slice + x, handles the dependency -------
         pdl_wait();
         pdl_trigger();
@@ -199,7 +278,8 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
             const uint32_t b = l & 1u;
             if (l >= 2) mbar_wait(&bempty[b], ((l >> 1) - 1) & 1u);
             const StackLayerDesc& d = layer_desc(p, l);
-            const uint32_t r0 = split_rows(d.rows, cta, G), r1 = split_rows(d.rows, cta + 1, G);
+            const Share sh = cta_share(d, cta);
+            const uint32_t r0 = sh.r0, r1 = sh.r0 + sh.n;
             uint8_t* xb = sm + p.off_x + b * p.x_bytes;
             if (lane == 0) DSQ_TRACE(l, kTrLoaderStart);
             // x: one TMA bulk copy of the 16-byte-aligned body (+ scalar tail,
@@ -239,20 +319,21 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
         return;
     }
 
-    if (warp == 2) {
-        // ---------------- finisher: CSR rounds, row totals, y, grid signal ---
+    if (warp == NC + 2) {
+        // ---------------- finisher: row totals, y, grid signal ----------------
         pdl_wait();
         pdl_trigger();
         for (uint32_t l = 0; l < p.n_layers; ++l) {
             const uint32_t b = l & 1u, ph = (l >> 1) & 1u;
-            const float* segs = reinterpret_cast<const float*>(sm + p.off_seg) + size_t(b) * p.seg_rounds * 32;
-            const float* gseg = p.gseg + (size_t(cta) * 2 + b) * p.gseg_rounds * 32;
+            float* segs = reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_rounds * 32;
+            float* gseg = p.gseg + (size_t(cta) * 2 + b) * p.gseg_rounds * 32;
             const StackLayerDesc& d = layer_desc(p, l);
-            const uint32_t r0 = split_rows(d.rows, cta, G), r1 = split_rows(d.rows, cta + 1, G);
-            const uint32_t nrows = r1 - r0, S = d.nslices;
+            const Share sh = cta_share(d, cta);
+            const uint32_t r0 = sh.r0, nrows = sh.n, S = d.nslices;
             const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
             // row totals: dense slices in order, then the row's CSR rounds
             mbar_wait(&pfull[b], ph);
+            if (lane == 0) DSQ_TRACE(l, kTrAllDense);
             const uint32_t e0 = rp[0];
             const float* part = reinterpret_cast<const float*>(sm + p.off_part) +
                                 size_t(b) * p.part_rows * p.part_stride;
@@ -272,6 +353,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
             }
             __syncwarp();
             if (lane == 0) {
+                DSQ_TRACE(l, kTrFinalDone);
                 mbar_arrive(&pempty[b]);
                 mbar_arrive(&bempty[b]);
                 red_release_gpu_add(p.counters + l, 1u);
@@ -292,13 +374,13 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
     // ---------------- consumers: dense LUT products only ----------------------
     pdl_wait();
     pdl_trigger();
-    const uint32_t cw = warp - 3;
+    const uint32_t cw = warp;
     uint32_t slot = 0, phase = 0;
     for (uint32_t l = 0; l < p.n_layers; ++l) {
         const uint32_t b = l & 1u;
         const StackLayerDesc& d = layer_desc(p, l);
-        const uint32_t r0 = split_rows(d.rows, cta, G), r1 = split_rows(d.rows, cta + 1, G);
-        const uint32_t nrows = r1 - r0, S = d.nslices, rw = d.rw;
+        const Share sh = cta_share(d, cta);
+        const uint32_t nrows = sh.n, S = d.nslices, rw = d.rw, cr = d.chunk_rows;
         const uint32_t ng = d.ng;
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrConsStart);
         mbar_wait(&xfull[b], (l >> 1) & 1u);
@@ -307,10 +389,9 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
         const uint4* xb = reinterpret_cast<const uint4*>(sm + p.off_x + b * p.x_bytes);
         float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * p.part_stride;
 
-        const uint32_t nch = chunk_count(nrows, d.chunk_rows);
-        for (uint32_t ci = 0; ci < nch; ++ci) {
-            const uint32_t rbase = chunk_start(nrows, nch, ci);  // local row of chunk start
-            const uint32_t n = chunk_start(nrows, nch, ci + 1) - rbase;
+        for (uint32_t ci = 0; ci < sh.nch; ++ci) {
+            const uint32_t rbase = ci * cr;  // local row of chunk start
+            const uint32_t n = min(cr, nrows - rbase);
             mbar_wait(&full[slot], phase);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(slot) * p.slot_bytes);
             // (row, slice) pairs in slice-major order, an equal share per warp,
@@ -319,7 +400,10 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
             const uint32_t wr = (cw + ci + l) % kStackConsumers;
             uint32_t q = (wr * P) / kStackConsumers;
             const uint32_t q1 = ((wr + 1) * P) / kStackConsumers;
-            uint32_t cs = q / n;
+            // cs = q / n without an integer division
+            uint32_t cs = uint32_t(__fmul_rz(float(q), __frcp_rn(float(n))));
+            if (cs * n > q) --cs;
+            if ((cs + 1) * n <= q) ++cs;
             uint32_t ra = q - cs * n;
             while (q < q1) {
                 const uint32_t rb_ = min(n, ra + (q1 - q));
@@ -328,22 +412,33 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
                 uint4 xv[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) xv[j] = gv ? xb[g * 4 + j] : make_uint4(0, 0, 0, 0);
+                float* pcol = part + cs;
+                uint32_t rr = ra;
                 const uint32_t* rowp = chunk + size_t(ra) * rw;
-                for (uint32_t rr = ra; rr < rb_; rr += 4, rowp += 4 * rw) {
+                for (; rr + 4 <= rb_; rr += 4, rowp += 4 * rw) {
+                    RowOps<BITS> ops[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) load_row<BITS>(rowp + i * rw, g, gv, ops[i]);
                     float v[4];
-                    if (rr + 4 <= rb_ && gv) {
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) v[i] = row_slice_dot<BITS>(rowp + i * rw, g, xv);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            v[i] = (rr + i < rb_ && gv) ? row_slice_dot<BITS>(rowp + i * rw, g, xv)
-                                                        : 0.f;
-                    }
+                    for (int i = 0; i < 4; ++i) v[i] = row_dot<BITS>(ops[i], xv);
                     const float t = reduce4(v[0], v[1], v[2], v[3], lane);
-                    const uint32_t i = lane >> 3;
-                    if ((lane & 7) == 0 && rr + i < rb_)
-                        part[(rbase + rr + i) * p.part_stride + cs] = t;
+                    if ((lane & 7) == 0) pcol[(rbase + rr + (lane >> 3)) * p.part_stride] = t;
+                }
+                if (rr + 2 <= rb_) {
+                    RowOps<BITS> o0, o1;
+                    load_row<BITS>(rowp, g, gv, o0);
+                    load_row<BITS>(rowp + rw, g, gv, o1);
+                    const float t = reduce2(row_dot<BITS>(o0, xv), row_dot<BITS>(o1, xv), lane);
+                    if ((lane & 15) == 0) pcol[(rbase + rr + (lane >> 4)) * p.part_stride] = t;
+                    rr += 2;
+                    rowp += 2 * rw;
+                }
+                if (rr < rb_) {
+                    RowOps<BITS> o0;
+                    load_row<BITS>(rowp, g, gv, o0);
+                    const float t = reduce1(row_dot<BITS>(o0, xv));
+                    if (lane == 0) pcol[(rbase + rr) * p.part_stride] = t;
                 }
                 q += rb_ - ra;
                 ++cs;
@@ -358,46 +453,18 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
         }
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrDenseDone);
 
-        // ---- CSR deltas of rows [r0, r1): 32-entry rounds, segmented scan.
-        // Round j covers entries [32j, 32j+32) of the CTA's contiguous slice;
-        // a lane starts a segment where some row starts.  Row starts are
-        // found in parallel (each lane tests <= ceil(nrows/32) row pointers).
+        // CSR deltas: rounds distributed over the consumer warps
         mbar_wait(&cfull[b], (l >> 1) & 1u);
         {
-            const uint16_t* xh = reinterpret_cast<const uint16_t*>(xb);
             const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
             const uint32_t e0 = rp[0], nz = rp[nrows] - e0;
             const uint32_t* ent = nz <= p.csr_cap
                                       ? reinterpret_cast<const uint32_t*>(sm + p.off_csr) + b * p.csr_cap
                                       : d.csr + e0;
-            float* segs = reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_rounds * 32;
-            float* gseg = p.gseg + (size_t(cta) * 2 + b) * p.gseg_rounds * 32;
-            const uint32_t rounds = (nz + 31) / 32;
-            for (uint32_t j = cw; j < rounds; j += kStackConsumers) {
-                const uint32_t base = e0 + j * 32;
-                const uint32_t pi = j * 32 + lane;
-                float prod = 0.f;
-                if (pi < nz) {
-                    const uint32_t e = ent[pi];
-                    prod = fma_h(uint16_t(e >> 16), xh[e & 0xffffu], 0.f);
-                }
-                uint32_t mybits = 0;
-                for (uint32_t r = lane; r < nrows; r += 32) {
-                    const uint32_t a = rp[r];
-                    if (a >= base && a < base + 32 && a < rp[r + 1]) mybits |= 1u << (a - base);
-                }
-                const uint32_t heads = __reduce_or_sync(0xffffffffu, mybits);
-                const uint32_t upto = heads & (0xffffffffu >> (31 - lane));
-                const uint32_t seg0 = upto ? (31u - __clz(upto)) : 0u;
-                float v = prod;
-#pragma unroll
-                for (uint32_t off = 1; off < 32; off <<= 1) {
-                    const float t = __shfl_up_sync(0xffffffffu, v, off);
-                    if (lane >= seg0 + off) v += t;
-                }
-                float* dst = j < p.seg_rounds ? segs + j * 32 : gseg + (j - p.seg_rounds) * 32;
-                dst[lane] = v;
-            }
+            csr_rounds(rp, nrows, ent, reinterpret_cast<const uint16_t*>(xb),
+                       reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_rounds * 32,
+                       p.gseg + (size_t(cta) * 2 + b) * p.gseg_rounds * 32, p.seg_rounds, cw,
+                       kStackConsumers, lane);
         }
         __syncwarp();
         if (lane == 0) {
@@ -410,7 +477,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) stack_gemv(const __grid_cons
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3(kStackThreads);
+    cfg.blockDim = dim3((p.consumers + 3) * 32);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -418,11 +485,15 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static bool attr_done[2][64] = {};
+    static bool attr_done[6][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    const int bi = p.bits == 3 ? 0 : 1;
-    auto kern = p.bits == 3 ? stack_gemv<3> : stack_gemv<4>;
+    const int ci = p.consumers == 8 ? 0 : p.consumers == 16 ? 1 : 2;
+    const int bi = (p.bits == 3 ? 0 : 1) * 3 + ci;
+    using K = void (*)(StackParams);
+    static const K kerns[6] = {stack_gemv<3, 8>, stack_gemv<3, 16>, stack_gemv<3, 24>,
+                               stack_gemv<4, 8>, stack_gemv<4, 16>, stack_gemv<4, 24>};
+    const K kern = kerns[bi];
     if (dev < 0 || dev >= 64 || !attr_done[bi][dev]) {
         int max_optin = 0;
         cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);

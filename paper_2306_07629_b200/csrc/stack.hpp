@@ -21,8 +21,7 @@
 
 namespace sqz {
 
-constexpr int kStackConsumers = 16;                 // decode warps per CTA
-constexpr int kStackThreads = (kStackConsumers + 3) * 32;  // + producer, loader, finisher
+constexpr int kStackConsumersDefault = 16;  // decode warps per CTA (8/16/24; DSQ_STACK_CONSUMERS)
 constexpr uint32_t kNoDep = 0xffffffffu;
 constexpr uint32_t kInlineLayers = 8;  // layer descs carried in the launch params
 
@@ -38,7 +37,10 @@ struct StackLayerDesc {
     uint32_t dep;             // layer whose output is x (kNoDep: external input)
     uint32_t y_f16;
     uint32_t nslices;         // ceil(ng / 32)
-    uint32_t pad_;
+    // host-precomputed row split over the grid (no device division):
+    // CTA c owns rows [c*rq + min(c, rr), ...) -- rq or rq+1 rows -- cut into
+    // fixed chunks of chunk_rows (nch_lo / nch_hi chunks for rq / rq+1 rows)
+    uint32_t rq, rr, nch_lo, nch_hi;
 };
 
 struct StackParams {
@@ -50,6 +52,7 @@ struct StackParams {
     float* gseg;              // global spill for CSR round results [G][gseg_rounds][32]
     uint32_t gseg_rounds;
     uint32_t grid;            // CTAs (== SMs, all co-resident)
+    uint32_t consumers;       // decode warps per CTA (+ producer, loader, finisher warps)
     // dynamic shared memory carve-up (byte offsets)
     uint32_t off_ring, slot_bytes, n_slots;
     uint32_t off_x, x_bytes;         // two x buffers
@@ -74,6 +77,8 @@ enum : uint32_t {
     kTrCsrDone,          // consumer warp 0 passed the CSR rounds barrier
     kTrSignaled,         // completion counter bumped
     kTrProdFirst,        // producer issued the layer's first chunk
+    kTrAllDense,         // finisher: all consumer warps done (pfull)
+    kTrFinalDone,        // finisher: row totals stored (before the release)
     kTrSlots
 };
 

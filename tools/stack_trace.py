@@ -13,7 +13,9 @@ import numpy as np
 os.environ["DSQ_STACK_TRACE"] = "1"
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 SLOTS = ["ld_start", "csr_staged", "dep_met", "x_issued", "c_start", "x_ready", "dense_done",
-         "csr_done", "signaled", "prod_first"]
+         "csr_done", "signaled", "prod_first", "all_dense", "final_done"]
+SHOW = ["dep_met", "x_issued", "c_start", "x_ready", "dense_done", "all_dense", "final_done",
+        "signaled", "prod_first"]
 
 
 def main():
@@ -60,11 +62,11 @@ def main():
     t = buf.reshape(G, n, len(SLOTS)).astype(np.float64)
     t0 = t[t > 0].min()
     t = np.where(t > 0, (t - t0) / 1e3, np.nan)
-    print(f"{'layer':>5} {'shape':>11} " + " ".join(f"{s:>14}" for s in SLOTS))
+    print(f"{'layer':>5} {'shape':>11} " + " ".join(f"{s:>14}" for s in SHOW))
     for l in range(n):
         name, r, c = bench.SHAPES[l % 7]
         cells = []
-        for k in range(len(SLOTS)):
+        for k in [SLOTS.index(s) for s in SHOW]:
             col = t[:, l, k]
             cells.append(f"{np.nanmedian(col):6.2f}/{np.nanmax(col):6.2f}")
         print(f"{l:5d} {name:>4}{r:>5}x{c:<5} " + " ".join(f"{c:>14}" for c in cells))
