@@ -8,7 +8,7 @@ CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libdsq_cuda.so
 OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/api.o
 
-all: $(LIB) oracle
+all: $(LIB) oracle cxx-test
 
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/layout.hpp $(CSRC)/ptx.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/kernels.ptxas.log || (cat $(CSRC)/kernels.ptxas.log; false)
@@ -25,8 +25,23 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# C++ integration test against the reference's own headers/types (built only
+# where /root/reference exists; the binary travels to the GPU box)
+REFINC := /root/reference/proj/include
+CXXTEST := tests/cpp/test_cxx_wrapper
+ifneq ($(wildcard $(REFINC)/dsq/kernels.hpp),)
+cxx-test: $(CXXTEST)
+$(CXXTEST): tests/cpp/test_cxx_wrapper.cpp include/dsq_cuda.hpp include/dsq_cuda.h $(LIB) oracle
+	g++ -std=c++20 -O2 -w -I$(REFINC) -Iinclude -o $@ $< \
+	    -Loracle/_ref -ldsqref -L$(PKG) -ldsq_cuda -fopenmp -lz \
+	    -Wl,-rpath,'$$ORIGIN/../../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+else
+cxx-test:
+	@echo "reference headers absent; using prebuilt $(CXXTEST) if present"
+endif
+
 clean:
 	rm -f $(OBJS) $(LIB) $(CSRC)/*.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean cxx-test

@@ -1,0 +1,139 @@
+// dsq_cuda.hpp -- header-only C++ layer over the C ABI (dsq_cuda.h) with the
+// reference's hot-path signatures (include/dsq/kernels.hpp:17-79).
+//
+// It is templated on the caller's layer types instead of including the
+// reference headers, so a reference user passes their own dsq::PackedDense /
+// dsq::CsrMatrix / dsq::QuantizedLayer unchanged (fields used: bits, rows,
+// cols, groups_per_row, luts, payload; rows, cols, row_ptr, col_idx, values;
+// name, packed, sparse, hybrid_top_k -- packfmt.hpp:16-61, dns.hpp:14-24).
+//
+//   #include <dsq/kernels.hpp>
+//   #include "dsq_cuda.hpp"
+//   sqz::DeviceLayer dev(layer);                  // validate + re-tile + upload once
+//   std::vector<double> y = dev.fused(x);          // == dsq::fused_dns_matvec(layer, x)
+//   std::vector<double> y2 = sqz::fused_dns_matvec(layer, x);   // one-shot form
+//
+// Errors: a non-OK status is rethrown as sqz::Error whose errc() is the
+// reference's dsq::errc value (status - 1), so `static_cast<dsq::errc>(e.errc())`
+// reproduces dsq::Error and the CLI exit-code mapping (tools/dsq.cpp:399-411).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dsq_cuda.h"
+
+namespace sqz {
+
+class Error : public std::runtime_error {
+public:
+    Error(int status, const std::string& msg) : std::runtime_error(msg), status_(status) {}
+    int status() const { return status_; }
+    // dsq::errc ordinal (valid for status 1..15), -1 for device-only failures
+    int errc() const { return status_ >= 1 && status_ <= 15 ? status_ - 1 : -1; }
+
+private:
+    int status_;
+};
+
+inline void check(int rc) {
+    if (rc != DSQ_OK) throw Error(rc, dsq_cuda_last_error());
+}
+
+template <class Packed>
+dsq_packed_view packed_view(const Packed& p) {
+    dsq_packed_view v{};
+    v.bits = p.bits;
+    v.rows = p.rows;
+    v.cols = p.cols;
+    v.groups_per_row = p.groups_per_row;
+    v.luts_f32 = p.luts.data();
+    v.payload = p.payload.data();
+    v.payload_len = p.payload.size();
+    return v;
+}
+
+template <class Csr>
+dsq_csr_view csr_view(const Csr& s) {
+    dsq_csr_view v{};
+    v.rows = s.rows;
+    v.cols = s.cols;
+    v.nnz = s.row_ptr.empty() ? 0u : s.row_ptr.back();
+    v.row_ptr = s.row_ptr.data();
+    v.col_idx = s.col_idx.empty() ? nullptr : s.col_idx.data();
+    v.values_f32 = s.values.empty() ? nullptr : s.values.data();
+    return v;
+}
+
+template <class Layer>
+dsq_layer_view layer_view(const Layer& l) {
+    dsq_layer_view v{};
+    v.name = l.name.c_str();
+    v.rows = l.rows;
+    v.cols = l.cols;
+    v.packed = packed_view(l.packed);
+    v.sparse = csr_view(l.sparse);
+    v.hybrid_top_k = l.hybrid_top_k;
+    return v;
+}
+
+// Owning handle of one uploaded layer.
+class DeviceLayer {
+public:
+    template <class Layer>
+    explicit DeviceLayer(const Layer& l, int device = 0) {
+        const dsq_layer_view v = layer_view(l);
+        dsq_cuda_layer* h = nullptr;
+        check(dsq_cuda_layer_create(&v, device, &h));
+        h_.reset(h);
+        cols_ = l.cols;
+        rows_ = l.rows;
+    }
+    dsq_cuda_layer* get() const { return h_.get(); }
+
+    // host-vector products with the reference's signatures (fp32 x -> fp64 y)
+    std::vector<double> lut(const std::vector<float>& x) const { return run(DSQ_KERNEL_LUT, x); }
+    std::vector<double> csr(const std::vector<float>& x) const { return run(DSQ_KERNEL_CSR, x); }
+    std::vector<double> fused(const std::vector<float>& x) const { return run(DSQ_KERNEL_FUSED, x); }
+    std::vector<double> reference(const std::vector<float>& x) const {
+        return run(DSQ_KERNEL_REFERENCE, x);
+    }
+
+    // device-buffer product on a caller stream (cudaStream_t as void*)
+    void gemv(int kernel, const void* x, int x_dtype, void* y, int y_dtype, void* stream) const {
+        check(dsq_cuda_gemv(h_.get(), kernel, x, x_dtype, y, y_dtype, 1, stream));
+    }
+
+private:
+    struct Del {
+        void operator()(dsq_cuda_layer* h) const { dsq_cuda_layer_destroy(h); }
+    };
+    std::vector<double> run(int kernel, const std::vector<float>& x) const {
+        if (x.size() != cols_) throw Error(DSQ_E_SHAPE_MISMATCH, "dimension mismatch");
+        std::vector<double> y(rows_);
+        check(dsq_cuda_matvec_host(h_.get(), kernel, x.data(), y.data()));
+        return y;
+    }
+    std::unique_ptr<dsq_cuda_layer, Del> h_;
+    size_t cols_ = 0, rows_ = 0;
+};
+
+// One-shot forms (upload + product; keep a DeviceLayer for repeated calls).
+template <class Layer>
+std::vector<double> fused_dns_matvec(const Layer& l, const std::vector<float>& x) {
+    return DeviceLayer(l).fused(x);
+}
+template <class Layer>
+std::vector<double> csr_part_matvec(const Layer& l, const std::vector<float>& x) {
+    return DeviceLayer(l).csr(x);
+}
+
+inline uint64_t bytes_touched_estimate(uint32_t rows, uint32_t cols, uint32_t bits,
+                                       uint32_t group_size, uint64_t nnz) {
+    return dsq_bytes_touched_estimate(rows, cols, bits, group_size, nnz);
+}
+
+}  // namespace sqz

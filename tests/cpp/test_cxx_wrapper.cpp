@@ -1,0 +1,99 @@
+// C++ integration test: the reference's own types (dsq::QuantizedLayer built
+// by the reference's quantize_layer, pipeline.cpp:7-47) passed unchanged to
+// the B200 library through include/dsq_cuda.hpp, compared with the
+// reference's dsq::fused_dns_matvec / lut_matvec / csr_matvec.
+//
+// Built here against /root/reference/proj/include + oracle/_ref/libdsqref.so
+// (make cxx-test); the binary travels to the GPU box and is run by
+// tests/test_cxx_wrapper.py (GPU).  Exit code 0 = pass.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "dsq/kernels.hpp"
+#include "dsq/pipeline.hpp"
+#include "dsq/sensitivity.hpp"
+#include "dsq_cuda.hpp"
+
+namespace {
+
+float round_f16(float f) {
+    // round to the nearest fp16 value (the device stores fp16): via the
+    // library's own behaviour is not allowed here, so use a portable routine
+    if (f == 0.0f || !std::isfinite(f)) return f;
+    int e;
+    const float m = std::frexp(f, &e);              // f = m * 2^e, 0.5 <= |m| < 1
+    const int shift = e < -13 ? 24 + e : 11;  // mantissa bits kept (subnormals fewer)
+    const float q = std::ldexp(std::nearbyint(std::ldexp(m, shift)), -shift);
+    return std::ldexp(q, e);
+}
+
+int fail(const char* what, double v) {
+    std::printf("FAIL %s (%g)\n", what, v);
+    return 1;
+}
+
+double normwise(const std::vector<double>& a, const std::vector<double>& b) {
+    double d = 0, m = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        d = std::max(d, std::fabs(a[i] - b[i]));
+        m = std::max(m, std::fabs(b[i]));
+    }
+    return m > 0 ? d / m : d;
+}
+
+}  // namespace
+
+int main() {
+    using namespace dsq;
+    const uint32_t rows = 96, cols = 256;
+    Rng rng(7);
+    WeightMatrix w;
+    w.name = "wrapped";
+    w.rows = rows;
+    w.cols = cols;
+    w.values.resize(size_t(rows) * cols);
+    for (auto& v : w.values) v = float(rng.student_t(4.0));
+    SensitivityMap s = uniform_sensitivity(w.name, rows, cols);
+    for (auto& v : s.values) v = float(rng.uniform());
+    QuantizeOptions opt;
+    opt.cfg.bits = 3;
+    opt.cfg.sensitive_fraction = 0.0005;
+    opt.cfg.outlier_fraction = 0.004;
+    QuantizedLayer layer = quantize_layer(w, s, opt);
+    // fp16-exact centroids / deltas / x so the comparison is tolerance-tight
+    for (auto& v : layer.packed.luts) v = round_f16(v);
+    for (auto& v : layer.sparse.values) v = round_f16(v);
+    layer.hybrid = hybrid_split(layer.sparse, layer.hybrid_top_k);
+    std::vector<float> x(cols);
+    for (auto& v : x) v = round_f16(float(rng.normal()));
+
+    try {
+        sqz::DeviceLayer dev(layer);
+        const double e_fused = normwise(dev.fused(x), fused_dns_matvec(layer, x));
+        const double e_lut = normwise(dev.lut(x), lut_matvec(layer.packed, x));
+        const double e_csr = normwise(dev.csr(x), csr_matvec(layer.sparse, x));
+        const double e_once = normwise(sqz::fused_dns_matvec(layer, x), fused_dns_matvec(layer, x));
+        std::printf("normwise err fused %.3e lut %.3e csr %.3e one-shot %.3e\n", e_fused, e_lut,
+                    e_csr, e_once);
+        if (e_fused > 1e-5) return fail("fused", e_fused);
+        if (e_lut > 1e-5) return fail("lut", e_lut);
+        if (e_csr > 1e-5) return fail("csr", e_csr);
+        if (e_once > 1e-5) return fail("one-shot", e_once);
+        if (sqz::bytes_touched_estimate(rows, cols, 3, 0, layer.sparse.nnz()) !=
+            bytes_touched_estimate(layer))
+            return fail("bytes_touched_estimate", 0);
+        // error mapping: a dimension mismatch is dsq::errc::shape_mismatch
+        try {
+            dev.fused(std::vector<float>(cols + 1));
+            return fail("no error on bad x", 0);
+        } catch (const sqz::Error& e) {
+            if (e.errc() != int(errc::shape_mismatch)) return fail("errc mapping", e.errc());
+        }
+    } catch (const sqz::Error& e) {
+        std::printf("sqz::Error status %d: %s\n", e.status(), e.what());
+        return 2;
+    }
+    std::printf("PASS\n");
+    return 0;
+}

@@ -1,0 +1,27 @@
+"""Runs the C++ integration test (tests/cpp/test_cxx_wrapper.cpp): the
+reference's own dsq::QuantizedLayer passed to the B200 library through
+include/dsq_cuda.hpp and compared with dsq::fused_dns_matvec."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+BIN = Path(__file__).resolve().parent / "cpp" / "test_cxx_wrapper"
+
+
+def test_cxx_wrapper_binary_built():
+    if not Path("/root/reference/proj/include").exists() and not BIN.exists():
+        pytest.skip("reference headers absent and no prebuilt binary")
+    assert BIN.exists(), "make cxx-test"
+
+
+@pytest.mark.gpu
+def test_cxx_wrapper_against_reference():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if not BIN.exists():
+        pytest.skip("binary not built")
+    r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=120)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "PASS" in r.stdout

@@ -1,0 +1,118 @@
+"""Tensor-parallel sharding host logic (paper_2306_07629_b200.tp), world size 2
+over torch.distributed gloo on CPU: column-parallel shards + all_gather and
+row-parallel shards + all_reduce reproduce the unsharded reference product.
+The per-shard product is the oracle (CPU); the GPU variant of the same
+sharding is checked in test_gpu_parity-style below (single device)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Layer, make_layer, make_x, to_quantized_layer
+
+
+def as_oracle_layer(q):
+    p, s = q.packed, q.sparse
+    return Layer(p.bits, q.rows, q.cols, np.zeros(1, np.uint16), np.asarray(p.luts, np.float16),
+                 np.asarray(p.payload, np.uint8), np.asarray(s.row_ptr, np.uint32),
+                 np.asarray(s.col_idx, np.uint16), np.asarray(s.values, np.float16))
+
+
+def free_port():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _worker(rank, world, port, mode, rows, cols, bits, out_path):
+    import torch
+    import torch.distributed as dist
+    from oracle.oracle import Oracle
+    from paper_2306_07629_b200.tp import shard_cols, shard_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        L = make_layer(rows, cols, bits, 0.02, seed=77, skew="zipf")
+        q = to_quantized_layer(L)
+        x = make_x(cols, seed=5).astype(np.float32)
+        if mode == "rows":
+            sq, r0, r1 = shard_rows(q, rank, world)
+            part = o.fused_dns_matvec(as_oracle_layer(sq), x, 10)
+            # all_gather of the row slices (pad to equal length)
+            n = torch.tensor([r1 - r0])
+            sizes = [torch.zeros(1, dtype=torch.long) for _ in range(world)]
+            dist.all_gather(sizes, n)
+            m = max(int(t) for t in sizes)
+            buf = torch.zeros(m, dtype=torch.float64)
+            buf[: r1 - r0] = torch.from_numpy(part)
+            got = [torch.zeros(m, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(got, buf)
+            y = np.concatenate([g[: int(s)].numpy() for g, s in zip(got, sizes)])
+        else:
+            sq, c0, c1 = shard_cols(q, rank, world)
+            part = o.fused_dns_matvec(as_oracle_layer(sq), x[c0:c1], 10)
+            t = torch.from_numpy(part.copy())
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            y = t.numpy()
+        if rank == 0:
+            np.save(out_path, y)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode,rows,cols,bits", [("rows", 97, 256, 3), ("cols", 64, 320, 3),
+                                                 ("cols", 40, 200, 4), ("rows", 33, 64, 4)])
+def test_tp_world2_matches_unsharded(tmp_path, oracle, mode, rows, cols, bits):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "y.npy")
+    mp.spawn(_worker, args=(2, free_port(), mode, rows, cols, bits, out), nprocs=2, join=True)
+    y = np.load(out)
+    L = make_layer(rows, cols, bits, 0.02, seed=77, skew="zipf")
+    x = make_x(cols, seed=5).astype(np.float32)
+    ref = oracle.fused_dns_matvec(L, x, 10)
+    if mode == "rows":
+        assert np.array_equal(y, ref)  # rows are independent: bit-exact
+    else:
+        np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_shard_cols_repack_roundtrip(oracle):
+    """Column shards re-pack the reference layout exactly (unpack of the shard
+    == the column slice of the unpacked layer)."""
+    from paper_2306_07629_b200.tp import shard_cols
+    L = make_layer(50, 300, 3, 0.01, seed=3)
+    q = to_quantized_layer(L)
+    rc, full = oracle.unpack(L.payload, 3, 50, 300)
+    full = full.reshape(50, 300)
+    for world in (2, 3, 4):
+        for r in range(world):
+            sq, c0, c1 = shard_cols(q, r, world)
+            rc, a = oracle.unpack(sq.packed.payload, 3, 50, c1 - c0)
+            assert rc == 0
+            assert np.array_equal(a.reshape(50, c1 - c0), full[:, c0:c1])
+            assert c0 % 32 == 0
+
+
+@pytest.mark.gpu
+def test_tp_shards_on_device(oracle):
+    """Every shard runs through the device path; recombined == unsharded."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2306_07629_b200 import fused_dns_matvec
+    from paper_2306_07629_b200.tp import shard_cols, shard_rows
+    L = make_layer(512, 1024, 3, 0.0045, seed=8)
+    q = to_quantized_layer(L)
+    x = make_x(1024, seed=9).astype(np.float32)
+    ref = oracle.fused_dns_matvec(L, x, 10)
+    for world in (2, 4, 8):
+        y = np.concatenate([fused_dns_matvec(shard_rows(q, r, world)[0], x) for r in range(world)])
+        assert np.abs(y - ref).max() <= 1e-5 * np.abs(ref).max()
+        yc = np.zeros_like(ref)
+        for r in range(world):
+            sq, c0, c1 = shard_cols(q, r, world)
+            yc += fused_dns_matvec(sq, x[c0:c1])
+        assert np.abs(yc - ref).max() <= 1e-5 * np.abs(ref).max()
