@@ -31,9 +31,9 @@ cudaError_t launch_decode(int mode, const LayerParams& P, void* out, cudaStream_
 cudaError_t launch_f32_to_f16(const float* in, uint16_t* out, uint32_t n, cudaStream_t st,
                               bool pdl);
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl);
-cudaError_t launch_decode_records(int mode, uint32_t bits, const uint32_t* rec, uint32_t rows,
-                                  uint32_t cols, uint32_t ng, uint32_t ngp, uint32_t rw,
-                                  void* out, cudaStream_t st);
+cudaError_t launch_decode_tiles(int mode, uint32_t bits, const uint32_t* idx, const uint32_t* lut,
+                                uint32_t rows, uint32_t cols, uint32_t ns, void* out,
+                                cudaStream_t st);
 }  // namespace sqz
 
 using namespace sqz;
@@ -167,32 +167,41 @@ int query_num_sms(int device, int* out) {
 namespace {
 
 struct StackPlanLayer {
-    uint32_t rows, cols, ng, ngp, rw, max_nnz_cta;
+    uint32_t rows, cols, tiles, ns, max_nnz_cta;
 };
 
+// CTA c of G owns tiles [c*tq + min(c, tr), ...): tq or tq+1 tiles
+inline void tile_share(uint32_t tiles, int G, uint32_t c, uint32_t& t0, uint32_t& nt) {
+    const uint32_t tq = tiles / uint32_t(G), tr = tiles % uint32_t(G);
+    t0 = c * tq + std::min(c, tr);
+    nt = tq + (c < tr ? 1u : 0u);
+}
+
 uint32_t max_nnz_per_cta(const std::vector<uint32_t>& rp, uint32_t rows, int G) {
+    const uint32_t tiles = ceil_div(rows, kTileRows);
     uint32_t m = 0;
     for (int c = 0; c < G; ++c) {
-        const uint32_t r0 = uint32_t((uint64_t(rows) * c) / G);
-        const uint32_t r1 = uint32_t((uint64_t(rows) * (c + 1)) / G);
+        uint32_t t0, nt;
+        tile_share(tiles, G, uint32_t(c), t0, nt);
+        const uint32_t r0 = std::min(t0 * kTileRows, rows);
+        const uint32_t r1 = std::min((t0 + nt) * kTileRows, rows);
         m = std::max(m, rp[r1] - rp[r0]);
     }
     return m;
 }
 
-void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, int G) {
-    d.rq = l.rows / uint32_t(G);
-    d.rr = l.rows % uint32_t(G);
+void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, uint32_t bits,
+               int G) {
+    d.tq = l.tiles / uint32_t(G);
+    d.tr = l.tiles % uint32_t(G);
     d.rows = l.rows;
     d.cols = l.cols;
-    d.ng = l.ng;
-    d.ngp = l.ngp;
-    d.rw = l.rw;
-    d.chunk_rows = std::max<uint32_t>(1, slot_bytes / (l.rw * 4));
-    d.nslices = ceil_div(l.ng, 32);
+    d.tiles = l.tiles;
+    d.ns = l.ns;
+    d.cu = slot_bytes / (unit_words(bits) * 4);
     d.dep = kNoDep;
-    d.nch_lo = ceil_div(d.rq, d.chunk_rows);
-    d.nch_hi = ceil_div(d.rq + 1, d.chunk_rows);
+    d.nch_lo = ceil_div(uint64_t(d.tq) * l.ns, d.cu);
+    d.nch_hi = ceil_div(uint64_t(d.tq + 1) * l.ns, d.cu);
 }
 
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
@@ -200,50 +209,59 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     int dev = 0, smax = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    uint32_t max_ng = 0, max_rows = 0, max_sl = 0, max_nnz = 0, max_rec = 0;
+    sp.consumers = kStackConsumersDefault;
+    if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
+        const int c = atoi(e);
+        if (c == 8 || c == 16 || c == 24) sp.consumers = uint32_t(c);
+    }
+    uint32_t max_ns = 0, max_rows = 0, max_nnz = 0;
     for (uint32_t i = 0; i < n; ++i) {
-        max_ng = std::max(max_ng, Ls[i].ng);
-        max_rows = std::max(max_rows, ceil_div(Ls[i].rows, G));
-        max_sl = std::max(max_sl, ceil_div(Ls[i].ng, 32));
+        max_ns = std::max(max_ns, Ls[i].ns);
+        max_rows = std::max(max_rows, ceil_div(Ls[i].tiles, G) * kTileRows);
         max_nnz = std::max(max_nnz, Ls[i].max_nnz_cta);
-        max_rec = std::max(max_rec, Ls[i].rw * 4);
     }
     auto al = [](size_t b, size_t a) { return (b + a - 1) / a * a; };
     size_t off = 1024;  // mbarriers
+    sp.off_desc = uint32_t(off);
+    off += 8 * 128;     // descriptor cache (stack.cu)
     sp.off_x = uint32_t(off);
-    sp.x_bytes = uint32_t(al(size_t(max_ng) * 64, 128));
+    sp.x_bytes = uint32_t(al(size_t(max_ns) * kSpanCols * 2, 128));
     off += 2 * size_t(sp.x_bytes);
+    sp.off_lut = uint32_t(off);
+    sp.lut_bytes = uint32_t(al(size_t(max_rows) * tile_lut_words(bits) * 4, 128));
+    off += 2 * size_t(sp.lut_bytes);
     sp.off_rp = uint32_t(off);
     sp.rp_words = uint32_t(al(max_rows + 1, 32));
     off += 2 * size_t(sp.rp_words) * 4;
     sp.off_csr = uint32_t(off);
     sp.csr_cap = uint32_t(al(std::min<uint32_t>(std::max<uint32_t>(max_nnz, 32), 2048), 32));
     off += 2 * size_t(sp.csr_cap) * 4;
+    sp.off_hb = uint32_t(off);
+    sp.hb_words = (sp.csr_cap / 32 + 16 + 3) & ~3u;  // 16-byte aligned TMA destinations
+    off += 2 * size_t(sp.hb_words) * 4;
     sp.off_part = uint32_t(off);
-    sp.part_stride = std::max<uint32_t>(max_sl, 1);
-    sp.part_rows = std::max<uint32_t>(max_rows, 1);
-    off = al(off + 2 * size_t(sp.part_rows) * sp.part_stride * 4, 128);
+    sp.part_rows = std::max<uint32_t>(max_rows, kTileRows);
+    off = al(off + 2 * size_t(sp.part_rows) * sp.consumers * 4, 128);
     sp.off_seg = uint32_t(off);
     const uint32_t rounds = (max_nnz + 31) / 32;
     sp.seg_rounds = std::min<uint32_t>(rounds, 32);
     off += 2 * size_t(sp.seg_rounds) * 128;
     gseg_rounds = rounds - sp.seg_rounds;
     sp.off_ring = uint32_t(al(off, 1024));
-    // big slots: a CTA's whole share of a 4096-column layer fits one chunk
-    sp.slot_bytes = uint32_t(al(std::max<uint32_t>(48 * 1024, max_rec), 128));
-    if (size_t(smax) < size_t(sp.off_ring) + 2 * size_t(sp.slot_bytes))
+    // the rest is the consumers' private rings: 2 slots per consumer warp,
+    // each a whole number of units (384 B 3-bit, 512 B 4-bit)
+    const uint32_t ub = unit_words(bits) * 4;
+    const size_t ring = size_t(smax) > sp.off_ring ? size_t(smax) - sp.off_ring : 0;
+    sp.n_slots = sp.consumers * 2;
+    sp.slot_bytes = uint32_t(ring / sp.n_slots / ub * ub);
+    if (sp.slot_bytes < 2 * ub)
         return fail(DSQ_E_UNSUPPORTED, "stack: layer too large for the shared-memory ring "
-                    "(x %u B, record %u B)", sp.x_bytes, max_rec);
-    sp.n_slots = std::min<uint32_t>((uint32_t(smax) - sp.off_ring) / sp.slot_bytes, 56);
+                    "(x %u B)", sp.x_bytes);
     sp.smem_bytes = sp.off_ring + sp.n_slots * sp.slot_bytes;
     sp.grid = uint32_t(G);
     sp.bits = bits;
-    sp.consumers = kStackConsumersDefault;
-    if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
-        const int c = atoi(e);
-        if (c == 8 || c == 16 || c == 24) sp.consumers = uint32_t(c);
-    }
-    for (uint32_t i = 0; i < n && i < kInlineLayers; ++i) fill_desc(sp.inl[i], Ls[i], sp.slot_bytes, G);
+    for (uint32_t i = 0; i < n && i < kInlineLayers; ++i)
+        fill_desc(sp.inl[i], Ls[i], sp.slot_bytes, bits, G);
     return DSQ_OK;
 }
 
@@ -268,11 +286,15 @@ struct dsq_cuda_layer {
     float* y32 = nullptr;       // host-API output staging
     float* x32 = nullptr;       // host-API input staging
     uint16_t* dense_w = nullptr;  // lazily materialized fp16 dense W (reference kernel)
-    // row-record layout (bits 3/4): the persistent stack kernel's format
+    // tile-record layout (bits 3/4): the persistent stack kernel's format
     bool rec_layout = false;
-    uint32_t ngp = 0, rw = 0;
+    uint32_t tiles = 0, ns = 0;
+    const uint32_t* tlut = nullptr;         // LUT planes [tiles][4][LW]
     const uint32_t* rec = nullptr;
     const uint32_t* zero_rp = nullptr;      // all-zero row_ptr (LUT-only products)
+    const uint32_t* csr_rng = nullptr;      // [num_sms][2] per-CTA CSR entry ranges
+    const uint32_t* zero_rng = nullptr;     // all-zero ranges (LUT-only products)
+    const uint32_t* csr_heads = nullptr;    // row-start bitmap of the CSR entries
     std::vector<uint32_t> row_ptr_host;
     StackParams sp1{};                      // single-layer stack plan
     uint32_t* stack_counters = nullptr;     // [2]
@@ -400,47 +422,59 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
     }
     const size_t stride = row_stride(cols, bits);
     const bool rec_layout = (bits == 3 || bits == 4);
-    const uint32_t ngp = (ng + 3) & ~3u;
-    const uint32_t lw = bits == 3 ? 4 : 8;
-    const uint32_t rw = rec_layout ? lw + bits * ngp : 0;
-    const size_t unit_words = size_t(bits) * 32;
+    const uint32_t ntiles = ceil_div(rows, kTileRows), ns = ceil_div(cols, kSpanCols);
+    const uint32_t lw = rec_layout ? tile_lut_words(bits) : 0;
+    const size_t unit_words_g = size_t(bits) * 32;
     const size_t n_units = size_t(n_rb) * ng;
-    std::vector<uint32_t> words;
+    std::vector<uint32_t> words, tluts;
     if (rec_layout) {
-        // ---- row records: [LUT byte planes][index words, k-major] (stack.hpp)
-        words.assign(size_t(rows) * rw, 0);
-#pragma omp parallel for schedule(dynamic, 16)
-        for (int64_t r = 0; r < int64_t(rows); ++r) {
+        // ---- tile layout: LUT planes [tiles][4][lw] + index units [tiles][ns][32 x bits] (stack.hpp)
+        words.assign(size_t(ntiles) * ns * unit_words(bits), 0);
+        tluts.assign(size_t(ntiles) * kTileRows * lw, 0);
+#pragma omp parallel for schedule(dynamic, 4)
+        for (int64_t tile = 0; tile < int64_t(ntiles); ++tile) {
             uint8_t idx[32];
             uint32_t w[8];
-            uint32_t* dst = words.data() + size_t(r) * rw;
-            const uint16_t* e = lut.data() + size_t(r) * K;
-            for (uint32_t set = 0; set < K / 8; ++set) {  // planes of entries 8*set .. 8*set+7
-                uint32_t l0 = 0, l1 = 0, h0 = 0, h1 = 0;
-                for (int i = 0; i < 4; ++i) {
-                    l0 |= uint32_t(e[8 * set + i] & 0xffu) << (8 * i);
-                    l1 |= uint32_t(e[8 * set + 4 + i] & 0xffu) << (8 * i);
-                    h0 |= uint32_t(e[8 * set + i] >> 8) << (8 * i);
-                    h1 |= uint32_t(e[8 * set + 4 + i] >> 8) << (8 * i);
+            for (uint32_t i = 0; i < kTileRows; ++i) {
+                const uint32_t r = uint32_t(tile) * kTileRows + i;
+                if (r >= rows) break;  // padded rows: zero LUT, index 0
+                const uint16_t* e = lut.data() + size_t(r) * K;
+                uint32_t* pl = tluts.data() + (size_t(tile) * kTileRows + i) * lw;
+                for (uint32_t set = 0; set < K / 8; ++set) {  // planes of entries 8*set .. 8*set+7
+                    uint32_t l0 = 0, l1 = 0, h0 = 0, h1 = 0;
+                    for (int q = 0; q < 4; ++q) {
+                        l0 |= uint32_t(e[8 * set + q] & 0xffu) << (8 * q);
+                        l1 |= uint32_t(e[8 * set + 4 + q] & 0xffu) << (8 * q);
+                        h0 |= uint32_t(e[8 * set + q] >> 8) << (8 * q);
+                        h1 |= uint32_t(e[8 * set + 4 + q] >> 8) << (8 * q);
+                    }
+                    pl[4 * set + 0] = l0;
+                    pl[4 * set + 1] = l1;
+                    pl[4 * set + 2] = h0;
+                    pl[4 * set + 3] = h1;
                 }
-                dst[4 * set + 0] = l0;
-                dst[4 * set + 1] = l1;
-                dst[4 * set + 2] = h0;
-                dst[4 * set + 3] = h1;
-            }
-            const uint8_t* row = v->packed.payload + size_t(r) * stride;
-            for (uint32_t g = 0; g < ng; ++g) {
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t c = g * kGroupCols + j;
-                    idx[j] = c < cols ? uint8_t(ref_index(row, stride, c, bits)) : 0;
+                const uint8_t* row = v->packed.payload + size_t(r) * stride;
+                for (uint32_t g = 0; g < ns * (kSpanCols / 32); ++g) {
+                    const uint32_t s = g / 8, gs = g % 8, h = gs >> 2, t = gs & 3;
+                    for (uint32_t j = 0; j < 32; ++j) {
+                        const uint32_t c = s * kSpanCols + tile_col(h, t, j);
+                        idx[j] = c < cols ? uint8_t(ref_index(row, stride, c, bits)) : 0;
+                    }
+                    encode_unit(idx, bits, w);
+                    const uint32_t lane = 16 * h + 4 * i + t;
+                    uint32_t* sp = words.data() + (size_t(tile) * ns + s) * unit_words(bits);
+                    for (uint32_t k = 0; k < bits; ++k) {
+                        if (bits == 3)
+                            sp[k * 32 + lane] = w[k];
+                        else
+                            sp[lane * 4 + k] = w[k];
+                    }
                 }
-                encode_unit(idx, bits, w);
-                for (uint32_t k = 0; k < bits; ++k) dst[lw + g * bits + k] = w[k];
             }
         }
     } else {
         // ---- tiled index words (generic widths, stream-K kernel)
-        words.assign(n_units * unit_words, 0);
+        words.assign(n_units * unit_words_g, 0);
 #pragma omp parallel for schedule(dynamic, 1)
         for (int64_t rb = 0; rb < int64_t(n_rb); ++rb) {
             uint8_t idx[32];
@@ -454,15 +488,15 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
                         idx[j] = (row && c < cols) ? uint8_t(ref_index(row, stride, c, bits)) : 0;
                     }
                     encode_unit(idx, bits, w);
-                    uint32_t* dst = words.data() + (size_t(rb) * ng + g) * unit_words;
+                    uint32_t* dst = words.data() + (size_t(rb) * ng + g) * unit_words_g;
                     for (uint32_t k = 0; k < bits; ++k) dst[k * 32 + lane] = w[k];
                 }
             }
         }
     }
     L->rec_layout = rec_layout;
-    L->ngp = ngp;
-    L->rw = rw;
+    L->tiles = ntiles;
+    L->ns = ns;
     L->row_ptr_host.assign(v->sparse.row_ptr, v->sparse.row_ptr + rows + 1);
     // ---- CSR entries: col | fp16(delta) << 16
     std::vector<uint32_t> csr(std::max<uint32_t>(L->nnz, 1), 0);
@@ -529,27 +563,33 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
         // ---- one arena
         auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
         const size_t o_words = 0;
-        const size_t o_lut = o_words + al(words.size() * 4);
+        const size_t o_tlut = o_words + al(words.size() * 4);
+        const size_t o_lut = o_tlut + al(tluts.size() * 4 + 16);
         const size_t o_rowptr = o_lut + al(lut.size() * 2);
-        const size_t o_csr = o_rowptr + al((size_t(rows) + 1) * 4);
-        const size_t o_scratch = o_csr + al(csr.size() * 4);
+        // row_ptr / CSR padded by 16 B: the stack loader copies 16-byte granules
+        const size_t o_csr = o_rowptr + al((size_t(rows) + 1) * 4 + 16);
+        const size_t o_scratch = o_csr + al(csr.size() * 4 + 16);
         const size_t o_counters = o_scratch + al(scratch_floats * 4);
         const size_t o_x16 = o_counters + al(size_t(n_rb) * 4);
         const size_t o_x32 = o_x16 + al((size_t(ng) * kGroupCols + 8) * 2);
         const size_t o_y32 = o_x32 + al(size_t(cols) * 4);
         const size_t o_zrp = o_y32 + al(size_t(rows) * 4);
-        const size_t o_scnt = o_zrp + al((size_t(rows) + 1) * 4);
+        const size_t o_scnt = o_zrp + al((size_t(rows) + 1) * 4 + 16);
+        const size_t heads_words = size_t(L->nnz) / 32 + 8;  // row-start bitmap (+pad)
+        const size_t o_heads = o_scnt + al(2 * 4);
+        const size_t o_rng = o_heads + al(heads_words * 4);   // per-CTA CSR entry ranges
+        const size_t o_zrng = o_rng + al(size_t(num_sms) * 8);  // all-zero ranges (LUT-only)
         // single-layer stack plan (bits 3/4)
         uint32_t gseg_rounds = 0;
         if (rec_layout) {
-            StackPlanLayer pl{rows, cols, ng, ngp, rw, max_nnz_per_cta(L->row_ptr_host, rows, num_sms)};
+            StackPlanLayer pl{rows, cols, ntiles, ns, max_nnz_per_cta(L->row_ptr_host, rows, num_sms)};
             int prc = plan_stack(&pl, 1, num_sms, bits, L->sp1, gseg_rounds);
             if (prc) {
                 delete L;
                 return prc;
             }
         }
-        const size_t o_gseg = o_scnt + al(2 * 4);
+        const size_t o_gseg = o_zrng + al(size_t(num_sms) * 8);
         const size_t total_bytes = o_gseg + al(size_t(num_sms) * 2 * gseg_rounds * 32 * 4 + 4);
         cudaError_t e = cudaMalloc(&L->arena, total_bytes);
         if (e != cudaSuccess) {
@@ -578,27 +618,53 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
         L->zero_rp = reinterpret_cast<const uint32_t*>(base + o_zrp);
         L->stack_counters = reinterpret_cast<uint32_t*>(base + o_scnt);
         L->gseg1 = reinterpret_cast<float*>(base + o_gseg);
+        L->csr_rng = reinterpret_cast<const uint32_t*>(base + o_rng);
+        L->zero_rng = reinterpret_cast<const uint32_t*>(base + o_zrng);
+        L->csr_heads = reinterpret_cast<const uint32_t*>(base + o_heads);
+        std::vector<uint32_t> heads(heads_words, 0);
+        for (uint32_t r = 0; r < rows; ++r) {
+            const uint32_t q = v->sparse.row_ptr[r];
+            if (q < v->sparse.row_ptr[r + 1]) heads[q >> 5] |= 1u << (q & 31);
+        }
+        // CTA c's CSR entries are [row_ptr[r0], row_ptr[r1]) of its tile rows
+        std::vector<uint32_t> rng(size_t(num_sms) * 2, 0);
+        for (int c = 0; c < num_sms; ++c) {
+            uint32_t t0, nt;
+            tile_share(ntiles, num_sms, uint32_t(c), t0, nt);
+            const uint32_t r0 = std::min(t0 * kTileRows, rows);
+            const uint32_t r1 = std::min((t0 + nt) * kTileRows, rows);
+            rng[2 * c] = v->sparse.row_ptr[r0];
+            rng[2 * c + 1] = v->sparse.row_ptr[r1];
+        }
         if (rec_layout) {
             L->rec = reinterpret_cast<const uint32_t*>(base + o_words);
+            L->tlut = reinterpret_cast<const uint32_t*>(base + o_tlut);
             StackParams& sp = L->sp1;
             sp.counters = L->stack_counters;
             sp.gseg = L->gseg1;
             sp.gseg_rounds = gseg_rounds;
             StackLayerDesc& d = sp.inl[0];
-            d.rec = L->rec;
+            d.idx = L->rec;
+            d.lut = L->tlut;
             d.row_ptr = P.row_ptr;
             d.csr = P.csr;
+            d.csr_rng = L->csr_rng;
+            d.csr_heads = L->csr_heads;
         }
         auto up = [&](size_t off, const void* src, size_t n) {
             return cudaMemcpy(base + off, src, n, cudaMemcpyHostToDevice);
         };
         if ((e = up(o_words, words.data(), words.size() * 4)) != cudaSuccess ||
+            (tluts.size() && (e = up(o_tlut, tluts.data(), tluts.size() * 4)) != cudaSuccess) ||
             (e = up(o_lut, lut.data(), lut.size() * 2)) != cudaSuccess ||
             (e = up(o_rowptr, v->sparse.row_ptr, (size_t(rows) + 1) * 4)) != cudaSuccess ||
             (e = up(o_csr, csr.data(), csr.size() * 4)) != cudaSuccess ||
             (e = cudaMemset(base + o_counters, 0, size_t(n_rb) * 4)) != cudaSuccess ||
             (e = cudaMemset(base + o_zrp, 0, (size_t(rows) + 1) * 4)) != cudaSuccess ||
             (e = cudaMemset(base + o_scnt, 0, 2 * 4)) != cudaSuccess ||
+            (e = up(o_rng, rng.data(), rng.size() * 4)) != cudaSuccess ||
+            (e = up(o_heads, heads.data(), heads.size() * 4)) != cudaSuccess ||
+            (e = cudaMemset(base + o_zrng, 0, size_t(num_sms) * 8)) != cudaSuccess ||
             (e = cudaMemset(base + o_x16, 0, (size_t(ng) * kGroupCols + 8) * 2)) != cudaSuccess ||
             (e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking)) != cudaSuccess) {
             cudaFree(L->arena);
@@ -641,8 +707,8 @@ static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
     if (L->dense_w) return DSQ_OK;
     CUDA_TRY(cudaMalloc(&L->dense_w, size_t(L->rows) * L->cols * 2));
     if (L->rec_layout)
-        CUDA_TRY(launch_decode_records(1, L->bits, L->rec, L->rows, L->cols, L->ng, L->ngp,
-                                       L->rw, L->dense_w, st));
+        CUDA_TRY(launch_decode_tiles(1, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns,
+                                     L->dense_w, st));
     else
         CUDA_TRY(launch_decode(1, L->P, L->dense_w, st));
     return DSQ_OK;
@@ -683,7 +749,10 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
         d.x = x16;
         d.y = y;
         d.y_f16 = yh ? 1u : 0u;
-        if (mode == 0) d.row_ptr = L->zero_rp;  // LUT part only: empty CSR
+        if (mode == 0) {  // LUT part only: empty CSR
+            d.row_ptr = L->zero_rp;
+            d.csr_rng = L->zero_rng;
+        }
         sp.n_layers = 1;
         sp.layers = nullptr;
         CUDA_TRY(launch_stack(sp, st, pdl));
@@ -751,8 +820,8 @@ int dsq_cuda_unpack(const dsq_cuda_layer* L, uint16_t* assign_dev, void* stream)
     if (!L || !assign_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     cudaSetDevice(L->device);
     if (L->rec_layout)
-        CUDA_TRY(launch_decode_records(0, L->bits, L->rec, L->rows, L->cols, L->ng, L->ngp,
-                                       L->rw, assign_dev, static_cast<cudaStream_t>(stream)));
+        CUDA_TRY(launch_decode_tiles(0, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns,
+                                     assign_dev, static_cast<cudaStream_t>(stream)));
     else
         CUDA_TRY(launch_decode(0, L->P, assign_dev, static_cast<cudaStream_t>(stream)));
     return DSQ_OK;
@@ -765,8 +834,8 @@ int dsq_cuda_dequant(const dsq_cuda_layer* L, void* w_dev, int out_dtype, void* 
     cudaSetDevice(L->device);
     const int mode = out_dtype == DSQ_F16 ? 1 : 2;
     if (L->rec_layout)
-        CUDA_TRY(launch_decode_records(mode, L->bits, L->rec, L->rows, L->cols, L->ng, L->ngp,
-                                       L->rw, w_dev, static_cast<cudaStream_t>(stream)));
+        CUDA_TRY(launch_decode_tiles(mode, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns,
+                                     w_dev, static_cast<cudaStream_t>(stream)));
     else
         CUDA_TRY(launch_decode(mode, L->P, w_dev, static_cast<cudaStream_t>(stream)));
     return DSQ_OK;
@@ -796,7 +865,7 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
         if (!L) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null layer %u", i);
         if (!L->rec_layout || L->bits != L0->bits)
             return fail(DSQ_E_UNSUPPORTED, "stack: layers must all be 3-bit or all 4-bit");
-        if (L->device != L0->device)
+        if (L->device != L0->device || L->num_sms != L0->num_sms)
             return fail(DSQ_E_INVALID_ARGUMENT, "stack: layers on different devices");
         if (deps[i] >= 0) {
             if (uint32_t(deps[i]) >= i)
@@ -809,7 +878,7 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
             return fail(DSQ_E_INVALID_ARGUMENT, "stack: x %u must be a 16-byte aligned fp16 buffer", i);
         }
         if (!ys[i]) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null y %u", i);
-        pl[i] = StackPlanLayer{L->rows, L->cols, L->ng, L->ngp, L->rw,
+        pl[i] = StackPlanLayer{L->rows, L->cols, L->tiles, L->ns,
                                max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
     }
     CUDA_TRY(cudaSetDevice(L0->device));
@@ -825,11 +894,14 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
     std::vector<StackLayerDesc> descs(n);
     for (uint32_t i = 0; i < n; ++i) {
         StackLayerDesc& d = descs[i];
-        fill_desc(d, pl[i], S->sp.slot_bytes, L0->num_sms);
+        fill_desc(d, pl[i], S->sp.slot_bytes, L0->bits, L0->num_sms);
         const dsq_cuda_layer* L = layers[i];
-        d.rec = L->rec;
+        d.idx = L->rec;
+        d.lut = L->tlut;
         d.row_ptr = L->P.row_ptr;
         d.csr = L->P.csr;
+        d.csr_rng = L->csr_rng;
+        d.csr_heads = L->csr_heads;
         d.dep = deps[i] >= 0 ? uint32_t(deps[i]) : kNoDep;
         d.x = deps[i] >= 0 ? static_cast<const uint16_t*>(ys[deps[i]])
                            : static_cast<const uint16_t*>(xs[i]);
@@ -859,9 +931,12 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
     S->sp.gseg_rounds = gseg_rounds;
     S->sp.n_layers = n;
     S->sp.trace = nullptr;
+    S->sp.dbg = 0;
+    if (const char* t = std::getenv("DSQ_STACK_DBG")) S->sp.dbg = uint32_t(atoi(t));
     if (const char* t = std::getenv("DSQ_STACK_TRACE")) {
         if (t[0] == '1') {
-            const size_t tbytes = size_t(S->sp.grid) * n * kTrSlots * 8;
+            const size_t tbytes =
+                std::max<size_t>(size_t(S->sp.grid) * n * kTrSlots, size_t(S->sp.grid) * 24 * 5) * 8;
             if (cudaMalloc(&S->trace, tbytes) == cudaSuccess) {
                 cudaMemset(S->trace, 0, tbytes);
                 S->sp.trace = S->trace;
@@ -877,7 +952,8 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
 extern "C" uint64_t dsq_cuda_stack_trace(dsq_cuda_stack* S, unsigned long long* host,
                                          uint64_t cap) {
     if (!S || !S->trace) return 0;
-    const uint64_t n = uint64_t(S->sp.grid) * S->n * kTrSlots;
+    const uint64_t n = std::max<uint64_t>(uint64_t(S->sp.grid) * S->n * kTrSlots,
+                                          uint64_t(S->sp.grid) * 24 * 5);
     if (cap < n) return 0;
     cudaSetDevice(S->device);
     cudaMemcpy(host, S->trace, n * 8, cudaMemcpyDeviceToHost);

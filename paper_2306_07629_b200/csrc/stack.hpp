@@ -1,46 +1,76 @@
 // stack.hpp -- persistent multi-layer decode kernel ("stack"), shared by the
 // host (api.cpp) and the device (stack.cu).
 //
-// Row-record layout (bits 3/4, the path the stack kernel serves): every row r
-// of a layer is one contiguous record of RW 32-bit words
-//     [ LUT byte planes: 4 words (3-bit) | 8 words (4-bit) ]
-//     [ index words, group-major: word k of group g at LW + g*bits + k ]
-// where NG = ceil(cols/32) groups of 32 columns, NGP = NG rounded up to a
-// multiple of 4 (16-byte records), and a group's `bits` words carry its 32
-// indices in the encoding of layout.hpp.  Lanes of a warp take consecutive
-// groups; with a 3-word (3-bit) stride the 32 lanes hit 32 distinct banks
-// (gcd(3,32) = 1) and with a 4-word stride (4-bit) one LDS.128 per lane is a
-// conflict-free 4-wavefront load, each lane using immediate offsets only.
-// The LUT is stored as PRMT byte planes (lo bytes of e0..e3, e4..e7, hi bytes
-// of e0..e3, e4..e7 -- same 16 bytes as the fp16 LUT, pre-transposed) so no
-// per-row conversion is needed.  A CTA's share of a layer is a contiguous row
-// range, i.e. a contiguous byte range -> plain TMA bulk copies.
+// Tile layout (bits 3/4, the path the stack kernel serves).  Rows are grouped
+// in TILES of 4 (rows padded to a multiple of 4 with all-zero LUTs); columns
+// in SPANS of 256 (padded with index 0; x is zero-padded on chip).  A layer
+// is two arrays:
+//
+//   lut [tiles][4 rows][LW words]   LUT byte planes of each row
+//       LW = 4 (3-bit): lo bytes e0..e3 | lo e4..e7 | hi e0..e3 | hi e4..e7
+//       LW = 8 (4-bit): the same for entries 0..7, then for 8..15
+//   idx [tiles][NS spans][32 lanes x BITS words]   one UNIT = (tile, span)
+//       lane = 16*h + 4*i + t  (i = row of the tile, h = 0/1, t = 0..3)
+//       carries 32 indices of row i, columns 256*s + tile_col(h, t, q),
+//       q = 0..31, in the "nibble + spare" encoding of layout.hpp; word order
+//       3-bit: [k][lane] (three conflict-free LDS.32)
+//       4-bit: [lane][k] (one conflict-free LDS.128)
+//
+// The lane -> (row, columns) map is the A-fragment map of a block-diagonal
+// mma.sync.m16n8k16: A row m = 4*blk + i holds tile row i on piece set blk,
+// B column n = blk holds x on those pieces, so one HMMA covers 4 rows x 64
+// columns and D[4*blk + i][blk] are the 4 partial dot products (tile.cuh).
+// Bytes: exactly rows*cols*bits/8 + 16*rows (3-bit) for aligned shapes, the
+// reference's charged bytes (packfmt.cpp:98-121).  A CTA's share of a layer
+// is a contiguous tile range, so its units are one contiguous byte range of
+// idx (streamed in fixed-size chunks of whole units) and its LUT planes one
+// contiguous range of lut -> plain TMA bulk copies.
 #pragma once
 
 #include <cstdint>
+
+#ifdef __CUDACC__
+#define SQZ_HD __host__ __device__
+#else
+#define SQZ_HD
+#endif
 
 namespace sqz {
 
 constexpr int kStackConsumersDefault = 16;  // decode warps per CTA (8/16/24; DSQ_STACK_CONSUMERS)
 constexpr uint32_t kNoDep = 0xffffffffu;
 constexpr uint32_t kInlineLayers = 8;  // layer descs carried in the launch params
+constexpr uint32_t kTileRows = 4;
+constexpr uint32_t kSpanCols = 256;
+
+// span column (0..255) of index position q (0..31) of lane (h, i, t): the
+// lane covers pieces 4h+t (q < 16) and 8+4h+t (q >= 16); piece p is columns
+// 8p + [0,8) then 128 + 8p + [0,8)  (tile.cuh)
+SQZ_HD inline uint32_t tile_col(uint32_t h, uint32_t t, uint32_t q) {
+    const uint32_t piece = (q < 16 ? 0u : 8u) + 4u * h + t, pos = q & 15u;
+    return (pos < 8 ? 0u : 128u) + 8u * piece + (pos & 7u);
+}
+
+inline uint32_t tile_lut_words(uint32_t bits) { return bits == 3 ? 4u : 8u; }  // per row
+inline uint32_t unit_words(uint32_t bits) { return bits * 32u; }
 
 struct StackLayerDesc {
-    const uint32_t* rec;      // row records [rows][rw]
-    const uint32_t* row_ptr;  // CSR row pointers [rows+1]
-    const uint32_t* csr;      // CSR entries: col | fp16(delta) << 16
-    const uint16_t* x;        // fp16 input [cols]
-    void* y;                  // output [rows], fp16 or fp32
-    uint32_t rows, cols, ng, ngp;
-    uint32_t rw;              // words per row record
-    uint32_t chunk_rows;      // max rows per ring slot (CTA shares split evenly)
-    uint32_t dep;             // layer whose output is x (kNoDep: external input)
+    const uint32_t* idx;        // index units [tiles][ns][bits*32]
+    const uint32_t* lut;        // LUT planes [tiles][4][LW]
+    const uint32_t* row_ptr;    // CSR row pointers [rows+1]
+    const uint32_t* csr;        // CSR entries: col | fp16(delta) << 16
+    const uint32_t* csr_rng;    // per CTA {row_ptr[r0], row_ptr[r1]} of its rows [grid][2]
+    const uint32_t* csr_heads;  // bitmap: bit q set <=> entry q starts a row [nnz/32 + pad]
+    const uint16_t* x;          // fp16 input [cols]
+    void* y;                    // output [rows], fp16 or fp32
+    uint32_t rows, cols;
+    uint32_t tiles, ns;         // ceil(rows/4), ceil(cols/256)
+    uint32_t dep;               // layer whose output is x (kNoDep: external input)
     uint32_t y_f16;
-    uint32_t nslices;         // ceil(ng / 32)
-    // host-precomputed row split over the grid (no device division):
-    // CTA c owns rows [c*rq + min(c, rr), ...) -- rq or rq+1 rows -- cut into
-    // fixed chunks of chunk_rows (nch_lo / nch_hi chunks for rq / rq+1 rows)
-    uint32_t rq, rr, nch_lo, nch_hi;
+    // host-precomputed tile split over the grid (no device division):
+    // CTA c owns tiles [c*tq + min(c, tr), ...) -- tq or tq+1 tiles -- whose
+    // units are streamed in chunks of cu units (nch_lo / nch_hi chunks)
+    uint32_t tq, tr, cu, nch_lo, nch_hi;
 };
 
 struct StackParams {
@@ -54,13 +84,20 @@ struct StackParams {
     uint32_t grid;            // CTAs (== SMs, all co-resident)
     uint32_t consumers;       // decode warps per CTA (+ producer, loader, finisher warps)
     // dynamic shared memory carve-up (byte offsets)
+    uint32_t off_desc;               // 8 x 128-byte layer descriptor cache
     uint32_t off_ring, slot_bytes, n_slots;
     uint32_t off_x, x_bytes;         // two x buffers
+    uint32_t off_lut, lut_bytes;     // two LUT-plane buffers (the CTA's tiles)
     uint32_t off_rp, rp_words;       // two row_ptr slices
     uint32_t off_csr, csr_cap;       // two CSR entry buffers (entries)
-    uint32_t off_part, part_stride, part_rows;  // two per-(row, slice) partial buffers
+    uint32_t off_hb, hb_words;       // two row-start bitmap buffers (words)
+    uint32_t off_part, part_rows;    // two [consumers][part_rows] dense-partial buffers
     uint32_t off_seg, seg_rounds;    // CSR round scan results (rounds x 32 floats)
     uint32_t smem_bytes;
+    // dev-only experiment switches (DSQ_STACK_DBG): bit 0 skips the decode math
+    // (results are garbage; measures the streaming skeleton alone), bit 2
+    // records the consumer cycle profile into `trace`
+    uint32_t dbg;
     // optional timeline (null = off): [grid][n_layers][kTraceSlots] globaltimer ns
     unsigned long long* trace;
 };
@@ -73,7 +110,7 @@ enum : uint32_t {
     kTrXIssued,          // x TMA issued
     kTrConsStart,        // consumer warp 0 begins the layer
     kTrXReady,           // consumer warp 0 sees x
-    kTrDenseDone,        // consumer warp 0 finished its dense pairs
+    kTrDenseDone,        // consumer warp 0 finished its dense units
     kTrCsrDone,          // consumer warp 0 passed the CSR rounds barrier
     kTrSignaled,         // completion counter bumped
     kTrProdFirst,        // producer issued the layer's first chunk

@@ -34,6 +34,9 @@ __global__ void __launch_bounds__(256) k(int n, uint32_t seed, uint32_t* out, Cl
               :"+f"(a.x),"+f"(a.y),"+f"(a.z),"+f"(a.w):"r"(r[0]),"r"(r[1]),"r"(r[2]),"r"(r[3]),"r"(r[4]),"r"(r[5])); } }
         else if (OP==9) { asm volatile("fma.rn.f32 %0,%0,%1,0f3F800000;":"+f"(f[i]):"f"(f[(i+1)&7])); }
         else if (OP==10) { asm volatile("shf.r.wrap.b32 %0,%0,%1,%2;":"+r"(r[i]):"r"(r[(i+1)&7]),"r"(c2)); }
+        else if (OP==12) { asm volatile("mul.hi.u32 %0,%0,%1;":"+r"(r[i]):"r"(c2)); }
+        else if (OP==13) { asm volatile("{.reg .b16 l,h,o,one; mov.b16 one, 0x3C00; mov.b32 {l,h}, %0; mul.rn.f16 o, h, one; mov.b32 %0, {o,l};}":"+r"(r[i])); }
+        else if (OP==14) { asm volatile("mad.hi.u32 %0,%0,%1,%2;":"+r"(r[i]):"r"(c2),"r"(r[(i+1)&7])); }
         else if (OP==11) { asm volatile("add.u32 %0,%0,%1;":"+r"(r[i]):"r"(r[(i+1)&7])); }
       }
     }
@@ -44,7 +47,7 @@ __global__ void __launch_bounds__(256) k(int n, uint32_t seed, uint32_t* out, Cl
 }
 int main(){
   uint32_t* out; cudaMalloc(&out, 148*8*256*4); Clk* clk; cudaMalloc(&clk,sizeof(Clk));
-  const char* names[12]={"FFMA 3reg","FFMA2","FHFMA f32.f16","HFMA2 f16x2","cvt.f32.f16","PRMT","LOP3","IMAD","HMMA m16n8k16 (per-instr)","FFMA imm","SHF","IADD"};
+  const char* names[15]={"FFMA 3reg","FFMA2","FHFMA f32.f16","HFMA2 f16x2","cvt.f32.f16","PRMT","LOP3","IMAD","HMMA m16n8k16 (per-instr)","FFMA imm","SHF","IADD","IMAD.HI (mul.hi)","HMUL hi->lo","IMAD.HI+add"};
   auto run=[&](auto kern, int op){
     int grid=148*4, n=4000; kern<<<grid,256>>>(10,1,out,clk); cudaDeviceSynchronize();
     cudaEvent_t e0,e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -54,6 +57,6 @@ int main(){
     double ops=double(grid)*256*n*32*(op==8?0.25:1.0);
     printf("%-26s %.3f ms  %.2f GHz  %.1f lane-ops/clk/SM (%.2f warp-instr/clk/SM)\n",names[op],ms,ghz,ops/(ms*1e-3)/(ghz*1e9)/148, ops/32/(ms*1e-3)/(ghz*1e9)/148);
   };
-  run(k<0>,0);run(k<1>,1);run(k<2>,2);run(k<3>,3);run(k<4>,4);run(k<5>,5);run(k<6>,6);run(k<7>,7);run(k<8>,8);run(k<9>,9);run(k<10>,10);run(k<11>,11);
+  run(k<0>,0);run(k<1>,1);run(k<2>,2);run(k<3>,3);run(k<4>,4);run(k<5>,5);run(k<6>,6);run(k<7>,7);run(k<8>,8);run(k<9>,9);run(k<10>,10);run(k<11>,11);run(k<12>,12);run(k<13>,13);run(k<14>,14);
   return 0;
 }
