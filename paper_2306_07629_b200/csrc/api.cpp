@@ -205,14 +205,14 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, 
 }
 
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
-               uint32_t& gseg_rounds) {
+               uint32_t& gseg_cap) {
     int dev = 0, smax = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     sp.consumers = kStackConsumersDefault;
     if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
         const int c = atoi(e);
-        if (c == 8 || c == 16 || c == 24) sp.consumers = uint32_t(c);
+        if (c == 8 || c == 16) sp.consumers = uint32_t(c);
     }
     uint32_t max_ns = 0, max_rows = 0, max_nnz = 0;
     for (uint32_t i = 0; i < n; ++i) {
@@ -234,7 +234,7 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.rp_words = uint32_t(al(max_rows + 1, 32));
     off += 2 * size_t(sp.rp_words) * 4;
     sp.off_csr = uint32_t(off);
-    sp.csr_cap = uint32_t(al(std::min<uint32_t>(std::max<uint32_t>(max_nnz, 32), 2048), 32));
+    sp.csr_cap = uint32_t(al(std::min<uint32_t>(std::max<uint32_t>(max_nnz + 4, 32), 2048), 32));
     off += 2 * size_t(sp.csr_cap) * 4;
     sp.off_hb = uint32_t(off);
     sp.hb_words = (sp.csr_cap / 32 + 16 + 3) & ~3u;  // 16-byte aligned TMA destinations
@@ -243,10 +243,9 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.part_rows = std::max<uint32_t>(max_rows, kTileRows);
     off = al(off + 2 * size_t(sp.part_rows) * sp.consumers * 4, 128);
     sp.off_seg = uint32_t(off);
-    const uint32_t rounds = (max_nnz + 31) / 32;
-    sp.seg_rounds = std::min<uint32_t>(rounds, 32);
-    off += 2 * size_t(sp.seg_rounds) * 128;
-    gseg_rounds = rounds - sp.seg_rounds;
+    sp.seg_cap = sp.csr_cap + 128;  // one float per staged entry position (+ a round)
+    off += 2 * size_t(sp.seg_cap) * 4;
+    gseg_cap = max_nnz > sp.csr_cap - 4 ? uint32_t(al(max_nnz + 256, 4)) : 0;
     sp.off_ring = uint32_t(al(off, 1024));
     // the rest is the consumers' private rings: 2 slots per consumer warp,
     // each a whole number of units (384 B 3-bit, 512 B 4-bit)
@@ -580,17 +579,17 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
         const size_t o_rng = o_heads + al(heads_words * 4);   // per-CTA CSR entry ranges
         const size_t o_zrng = o_rng + al(size_t(num_sms) * 8);  // all-zero ranges (LUT-only)
         // single-layer stack plan (bits 3/4)
-        uint32_t gseg_rounds = 0;
+        uint32_t gseg_cap = 0;
         if (rec_layout) {
             StackPlanLayer pl{rows, cols, ntiles, ns, max_nnz_per_cta(L->row_ptr_host, rows, num_sms)};
-            int prc = plan_stack(&pl, 1, num_sms, bits, L->sp1, gseg_rounds);
+            int prc = plan_stack(&pl, 1, num_sms, bits, L->sp1, gseg_cap);
             if (prc) {
                 delete L;
                 return prc;
             }
         }
         const size_t o_gseg = o_zrng + al(size_t(num_sms) * 8);
-        const size_t total_bytes = o_gseg + al(size_t(num_sms) * 2 * gseg_rounds * 32 * 4 + 4);
+        const size_t total_bytes = o_gseg + al(size_t(num_sms) * 2 * gseg_cap * 4 + 4);
         cudaError_t e = cudaMalloc(&L->arena, total_bytes);
         if (e != cudaSuccess) {
             delete L;
@@ -642,7 +641,7 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
             StackParams& sp = L->sp1;
             sp.counters = L->stack_counters;
             sp.gseg = L->gseg1;
-            sp.gseg_rounds = gseg_rounds;
+            sp.gseg_cap = gseg_cap;
             StackLayerDesc& d = sp.inl[0];
             d.idx = L->rec;
             d.lut = L->tlut;
@@ -885,8 +884,8 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
     auto* S = new dsq_cuda_stack;
     S->device = L0->device;
     S->n = n;
-    uint32_t gseg_rounds = 0;
-    int rc = plan_stack(pl.data(), n, L0->num_sms, L0->bits, S->sp, gseg_rounds);
+    uint32_t gseg_cap = 0;
+    int rc = plan_stack(pl.data(), n, L0->num_sms, L0->bits, S->sp, gseg_cap);
     if (rc) {
         delete S;
         return rc;
@@ -911,7 +910,7 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
     }
     const size_t tb = (size_t(n) * sizeof(StackLayerDesc) + 255) & ~size_t(255);
     const size_t cb = ((size_t(n) + 1) * 4 + 255) & ~size_t(255);
-    const size_t gb = size_t(L0->num_sms) * 2 * gseg_rounds * 32 * 4 + 4;
+    const size_t gb = size_t(L0->num_sms) * 2 * gseg_cap * 4 + 4;
     cudaError_t e = cudaMalloc(&S->arena, tb + cb + gb);
     if (e != cudaSuccess) {
         delete S;
@@ -928,7 +927,7 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
     S->sp.layers = reinterpret_cast<const StackLayerDesc*>(base);
     S->sp.counters = reinterpret_cast<uint32_t*>(base + tb);
     S->sp.gseg = reinterpret_cast<float*>(base + tb + cb);
-    S->sp.gseg_rounds = gseg_rounds;
+    S->sp.gseg_cap = gseg_cap;
     S->sp.n_layers = n;
     S->sp.trace = nullptr;
     S->sp.dbg = 0;

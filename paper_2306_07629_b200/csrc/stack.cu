@@ -57,10 +57,11 @@ namespace sqz {
 // and re-reading them per field from every warp is slow.
 constexpr uint32_t kDescSlots = 8;
 constexpr uint32_t kWarpSlots = 2;  // ring slots per consumer warp
+constexpr uint32_t kCsrWarps = 4;   // warps that process the CSR deltas
 struct __align__(16) SDesc {
     StackLayerDesc d;
     uint32_t e0, e1;  // CSR entries of this CTA's rows: [e0, e1)
-    uint32_t pad[(128 - sizeof(StackLayerDesc) - 8) / 4];
+    uint32_t t0, nt;  // this CTA's tiles [t0, t0 + nt)
 };
 static_assert(sizeof(SDesc) == 128, "descriptor slot is one 128-byte line");
 
@@ -95,61 +96,68 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
             p.trace[(size_t(blockIdx.x) * p.n_layers + (l)) * kTrSlots + (slot)] = gtimer_ns(); \
     } while (0)
 
-// CSR deltas of the CTA's rows: 32-entry rounds j = first, first+stride, ...
-// of the CTA's contiguous entry slice.  hb is the host-built bitmap of row
-// starts (bit q = entry q begins a row), so a lane knows where its segment
-// begins without scanning row pointers; a segmented inclusive warp scan
-// (5 shuffles) then leaves each row's partial of the round at its last entry.
-// Two rounds are processed together for instruction-level parallelism.
-__device__ __forceinline__ void csr_round_pair(uint32_t e0, uint32_t nz, const uint32_t* ent,
-                                               const uint32_t* hb, uint32_t hbase,
-                                               const uint16_t* xh, float* segs, float* gseg,
-                                               uint32_t seg_rounds, uint32_t j0, uint32_t j1,
-                                               bool two, uint32_t lane) {
-    float v[2];
-    uint32_t seg0[2];
+// CSR deltas of the CTA's rows.  The entries [e0, e1) are addressed by
+// position p = q - ea (ea = e0 rounded down to 4, so every lane's 4-entry
+// chunk is one aligned 16-byte load).  A round is 128 positions: lane L takes
+// positions 4L..4L+3, forms the products and their running sums restarted at
+// row starts (hb: host-built bitmap, bit q set <=> entry q begins a row), and
+// one segmented warp scan over the lanes' open tails carries rows across
+// lanes.  Result: S[p] = sum of entry p's row's products from max(row start,
+// round start) through p -- the finishers read S at each row's last position
+// in every round the row touches.  Positions outside [e0, e1) count 0.
+__device__ __forceinline__ void csr_stream(uint32_t ea, uint32_t e0, uint32_t e1,
+                                           const uint32_t* ent, const uint32_t* hb,
+                                           uint32_t hbase, uint32_t hlast, const uint16_t* xh,
+                                           float* S, uint32_t first, uint32_t stride,
+                                           uint32_t lane) {
+    const uint32_t np = e1 - ea;
+    const uint32_t rounds = (np + 127) / 128;
+    for (uint32_t j = first; j < rounds; j += stride) {
+        const uint32_t p0 = j * 128 + 4 * lane;
+        const uint32_t g = ea + p0;  // global entry index of position p0
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t hbits = 0;
+        if (p0 < np) {
+            const uint4 e4 = *reinterpret_cast<const uint4*>(ent + p0);
+            const uint32_t es[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t j = k ? j1 : j0;
-        const uint32_t pi = j * 32 + lane;
-        v[k] = 0.f;
-        if ((k == 0 || two) && pi < nz) {
-            const uint32_t e = ent[pi];
-            v[k] = fma_h(uint16_t(e >> 16), xh[e & 0xffffu], 0.f);
+            for (int m = 0; m < 4; ++m)
+                if (g + m >= e0 && g + m < e1)
+                    v[m] = fma_h(uint16_t(es[m] >> 16), xh[es[m] & 0xffffu], 0.f);
+            const uint32_t wi = min((g >> 5) - hbase, hlast);
+            hbits = (__funnelshift_r(hb[wi], hb[wi + 1], g & 31u)) & 0xfu;
         }
-        const uint32_t g = e0 + j * 32, w = (g >> 5) - hbase;
-        const uint32_t heads = __funnelshift_r(hb[w], hb[w + 1], g & 31u);
-        const uint32_t upto = heads & (0xffffffffu >> (31 - lane));
-        seg0[k] = upto ? (31u - __clz(upto)) : 0u;
-    }
+        // running sums inside the chunk, restarted at row starts
+        float c[4];
+        c[0] = v[0];
 #pragma unroll
-    for (uint32_t off = 1; off < 32; off <<= 1) {
-        const float t0 = __shfl_up_sync(0xffffffffu, v[0], off);
-        const float t1 = __shfl_up_sync(0xffffffffu, v[1], off);
-        if (lane >= seg0[0] + off) v[0] += t0;
-        if (lane >= seg0[1] + off) v[1] += t1;
-    }
+        for (int m = 1; m < 4; ++m) c[m] = ((hbits >> m) & 1u) ? v[m] : c[m - 1] + v[m];
+        // segmented inclusive scan of the open tails across lanes
+        const uint32_t starts = __ballot_sync(0xffffffffu, hbits != 0);
+        const uint32_t upto = starts & (0xffffffffu >> (31 - lane));
+        const uint32_t seg0 = upto ? (31u - __clz(upto)) : 0u;
+        float incl = c[3];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        if (k == 1 && !two) break;
-        const uint32_t j = k ? j1 : j0;
-        float* dst = j < seg_rounds ? segs + j * 32 : gseg + (j - seg_rounds) * 32;
-        dst[lane] = v[k];
+        for (uint32_t off = 1; off < 32; off <<= 1) {
+            const float t = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= seg0 + off) incl += t;
+        }
+        float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = 0.f;
+        // positions before this lane's first row start continue the open row
+        const uint32_t first_head = hbits ? uint32_t(__ffs(hbits) - 1) : 4u;
+        float4 o;
+        o.x = c[0] + (0 < first_head ? excl : 0.f);
+        o.y = c[1] + (1 < first_head ? excl : 0.f);
+        o.z = c[2] + (2 < first_head ? excl : 0.f);
+        o.w = c[3] + (3 < first_head ? excl : 0.f);
+        if (p0 < np) *reinterpret_cast<float4*>(S + p0) = o;
     }
-}
-
-__device__ __forceinline__ void csr_rounds(uint32_t e0, uint32_t nz, const uint32_t* ent,
-                                           const uint32_t* hb, uint32_t hbase, const uint16_t* xh,
-                                           float* segs, float* gseg, uint32_t seg_rounds,
-                                           uint32_t first, uint32_t stride, uint32_t lane) {
-    const uint32_t rounds = (nz + 31) / 32;
-    for (uint32_t j = first; j < rounds; j += 2 * stride)
-        csr_round_pair(e0, nz, ent, hb, hbase, xh, segs, gseg, seg_rounds, j, j + stride,
-                       j + stride < rounds, lane);
 }
 
 template <int BITS, int NC>
-__global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_constant__ StackParams p) {
+__global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
+    stack_gemv(const __grid_constant__ StackParams p) {
     constexpr uint32_t LW = BITS == 3 ? 4u : 8u;   // LUT words per tile row
     constexpr uint32_t UW = BITS * 32u;             // words per (tile, span) unit
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -173,13 +181,13 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
         for (int b = 0; b < 2; ++b) {
             mbar_init(&xfull[b], 1);
             mbar_init(&cfull[b], 1);
-            mbar_init(&bempty[b], NC + 1);
-            mbar_init(&pfull[b], NC);
-            mbar_init(&pempty[b], 1);
+            mbar_init(&bempty[b], NC + 1 + kCsrWarps);
+            mbar_init(&pfull[b], NC + kCsrWarps);
+            mbar_init(&pempty[b], 1 + kCsrWarps);
         }
         for (uint32_t k = 0; k < kDescSlots; ++k) {
             mbar_init(&dfull[k], 32);
-            mbar_init(&dempty[k], NC + 2);
+            mbar_init(&dempty[k], NC + 2 + kCsrWarps);
         }
         fence_barrier_init();
     }
@@ -207,8 +215,14 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
             const StackLayerDesc& gd = layer_desc(p, l);
             uint32_t* dst = reinterpret_cast<uint32_t*>(&sdesc[k]);
             constexpr uint32_t kDW = sizeof(StackLayerDesc) / 4;
-            if (lane < kDW) dst[lane] = reinterpret_cast<const uint32_t*>(&gd)[lane];
-            else if (lane < kDW + 2) dst[lane] = gd.csr_rng[2 * cta + (lane - kDW)];
+            if (lane < kDW) {
+                dst[lane] = reinterpret_cast<const uint32_t*>(&gd)[lane];
+            } else if (lane < kDW + 2) {
+                dst[lane] = gd.csr_rng[2 * cta + (lane - kDW)];
+            } else if (lane < kDW + 4) {
+                const Share sh = cta_share(gd, cta);
+                dst[lane] = lane == kDW + 2 ? sh.t0 : sh.nt;
+            }
             mbar_arrive(&dfull[k]);
             __syncwarp();
         }
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
             }
             if (d.dep != kNoDep) {
                 if (lane == 0) {
-                    while (ld_acquire_gpu(p.counters + d.dep) < G) __nanosleep(20);
+                    while (ld_acquire_gpu(p.counters + d.dep) < G * (1 + kCsrWarps)) __nanosleep(20);
                     DSQ_TRACE(l, kTrDepMet);
                 }
                 __syncwarp();
@@ -291,65 +305,116 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
         return;
     }
 
-    if (warp == NC + 2) {
-        // ---------------- finisher: row totals, y, grid signal ----------------
-        pdl_wait();
-        pdl_trigger();
-        for (uint32_t l = 0; l < p.n_layers; ++l) {
-            const uint32_t b = l & 1u, ph = (l >> 1) & 1u;
-            float* segs = reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_rounds * 32;
-            float* gseg = p.gseg + (size_t(cta) * 2 + b) * p.gseg_rounds * 32;
-            const StackLayerDesc& d = desc_wait(l).d;
-            const Share sh = cta_share(d, cta);
-            const uint32_t r0 = sh.r0, nrows = sh.nrows;
-            const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
-            mbar_wait(&pfull[b], ph);
-            if (lane == 0) DSQ_TRACE(l, kTrAllDense);
-            const uint32_t e0 = rp[0];
-            float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * NC;
-            // row totals: dense partials in warp order (warps that did not
-            // touch a row left 0), then the row's CSR rounds in round order
-            for (uint32_t i = lane; i < sh.nt * kTileRows; i += 32) {
-                float s = 0.f;
+    // ---- finishing (finisher warp + the CSR warps, kFin warps): rows
+    // i = 32*f + lane (mod 32*kFin) of the layer get their dense partials in
+    // warp order (warps that did not touch a row left 0) plus their CSR
+    // rounds in round order, y is stored, and each finishing warp bumps the
+    // layer's completion counter (target grid * kFin)
+    constexpr uint32_t kFin = 1 + kCsrWarps;
+    auto finish_rows = [&](uint32_t l, uint32_t f) {
+        const uint32_t b = l & 1u, ph = (l >> 1) & 1u;
+        const SDesc& sd = sdesc[l % kDescSlots];
+        const StackLayerDesc& d = sd.d;
+        const Share sh = cta_share(d, cta);
+        const uint32_t r0 = sh.r0, nrows = sh.nrows;
+        const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
+        mbar_wait(&pfull[b], ph);
+        if (f == 0 && lane == 0) DSQ_TRACE(l, kTrAllDense);
+        // the CSR scan results (position-indexed, see csr_stream)
+        const uint32_t ea = sd.e0 & ~3u;
+        const float* S = sd.e1 - sd.e0 <= p.csr_cap - 4
+                             ? reinterpret_cast<const float*>(sm + p.off_seg) + size_t(b) * p.seg_cap
+                             : p.gseg + (size_t(cta) * 2 + b) * p.gseg_cap;
+        float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * NC;
+        for (uint32_t i = 32 * f + lane; i < sh.nt * kTileRows; i += 32 * kFin) {
+            float s = 0.f;
 #pragma unroll
-                for (uint32_t w = 0; w < NC; ++w) {
-                    s += part[w * p.part_rows + i];
-                    part[w * p.part_rows + i] = 0.f;
-                }
-                if (i >= nrows) continue;  // padding rows of the last tile
-                const uint32_t a = rp[i] - e0, e = rp[i + 1] - e0;
-                for (uint32_t j = a / 32; e > a && j <= (e - 1) / 32; ++j) {
-                    const uint32_t end = min(e - 1 - j * 32, 31u);
-                    const float* src = j < p.seg_rounds ? segs + j * 32 : gseg + (j - p.seg_rounds) * 32;
-                    s += src[end];
-                }
-                if (d.y_f16)
-                    static_cast<__half*>(d.y)[r0 + i] = __float2half_rn(s);
-                else
-                    static_cast<float*>(d.y)[r0 + i] = s;
+            for (uint32_t w = 0; w < NC; ++w) {
+                s += part[w * p.part_rows + i];
+                part[w * p.part_rows + i] = 0.f;
             }
-            __syncwarp();
-            if (lane == 0) {
-                DSQ_TRACE(l, kTrFinalDone);
-                mbar_arrive(&pempty[b]);
-                mbar_arrive(&bempty[b]);
-                red_release_gpu_add(p.counters + l, 1u);
-                DSQ_TRACE(l, kTrSignaled);
-            }
-            __syncwarp();
-            desc_release(l);
+            if (i >= nrows) continue;  // padding rows of the last tile
+            const uint32_t a = rp[i] - ea, e = rp[i + 1] - ea;
+            for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j)
+                s += S[j * 128 + min(e - 1 - j * 128, 127u)];
+            if (d.y_f16)
+                static_cast<__half*>(d.y)[r0 + i] = __float2half_rn(s);
+            else
+                static_cast<float*>(d.y)[r0 + i] = s;
         }
-        // the last CTA to finish resets the counters for the next launch
+        __syncwarp();
         if (lane == 0) {
+            if (f == 0) DSQ_TRACE(l, kTrFinalDone);
+            mbar_arrive(&pempty[b]);
+            mbar_arrive(&bempty[b]);
+            red_release_gpu_add(p.counters + l, 1u);
+            if (f == 0) DSQ_TRACE(l, kTrSignaled);
+        }
+        __syncwarp();
+    };
+    // the last finishing warp of the last CTA resets the counters for the
+    // next launch (all finishing warps of a CTA meet at named barrier 1)
+    auto finish_kernel = [&]() {
+        named_bar_sync(1, 32 * kFin);
+        if (warp == NC + 2 && lane == 0) {
             const uint32_t old = atomicAdd(p.counters + p.n_layers, 1u);
             if (old == G - 1) {
                 for (uint32_t l = 0; l <= p.n_layers; ++l) p.counters[l] = 0;
             }
         }
+    };
+
+    if (warp == NC + 2) {
+        // ---------------- finisher ----------------------------------------------
+        pdl_wait();
+        pdl_trigger();
+        for (uint32_t l = 0; l < p.n_layers; ++l) {
+            desc_wait(l);
+            finish_rows(l, 0);
+            desc_release(l);
+        }
+        finish_kernel();
         return;
     }
 
-    // ---------------- consumers: dense LUT products + CSR rounds --------------
+    if (warp >= NC + 3) {
+        // ---------------- CSR warps: the deltas of the CTA's rows, then finishing
+        pdl_wait();
+        pdl_trigger();
+        const uint32_t cw = warp - (NC + 3);
+        for (uint32_t l = 0; l < p.n_layers; ++l) {
+            const uint32_t b = l & 1u, ph = (l >> 1) & 1u;
+            const SDesc& sd = desc_wait(l);
+            const Share sh = cta_share(sd.d, cta);
+            mbar_wait(&xfull[b], ph);
+            mbar_wait(&cfull[b], ph);
+            if (l >= 2) mbar_wait(&pempty[b], ((l >> 1) - 1) & 1u);  // segs consumed
+            if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrStaged);
+            const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_bytes);
+            const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
+            (void)rp;
+            const uint32_t e0 = sd.e0, e1 = sd.e1, ea = e0 & ~3u;
+            const bool staged = e1 - e0 <= p.csr_cap - 4;
+            const uint32_t* ent = staged ? reinterpret_cast<const uint32_t*>(sm + p.off_csr) + b * p.csr_cap
+                                         : sd.d.csr + ea;
+            const uint32_t* hb = staged ? reinterpret_cast<const uint32_t*>(sm + p.off_hb) + b * p.hb_words
+                                        : sd.d.csr_heads;
+            const uint32_t hbase = staged ? ((e0 >> 5) & ~3u) : 0u;
+            const uint32_t hlast = staged ? p.hb_words - 2 : ((e1 + 31) >> 5) + 1;
+            float* S = staged ? reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_cap
+                              : p.gseg + (size_t(cta) * 2 + b) * p.gseg_cap;
+            if (e1 > e0) csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh, S, cw, kCsrWarps, lane);
+            __syncwarp();
+            if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrDone);
+            if (lane == 0) mbar_arrive(&pfull[b]);
+            finish_rows(l, 1 + cw);
+            desc_release(l);
+        }
+        finish_kernel();
+        return;
+    }
+
+    // ---------------- consumers: dense LUT products ----------------------------
     pdl_wait();
     pdl_trigger();
     const uint32_t cw = warp;
@@ -371,13 +436,12 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
         while (true) {
             if (!pvalid) {
                 if (pl >= p.n_layers) return;
-                const StackLayerDesc& dn = desc_wait(pl).d;
-                const Share shn = cta_share(dn, cta);
-                const uint32_t Un = shn.nt * dn.ns;
+                const SDesc& sn = desc_wait(pl);
+                const uint32_t Un = sn.nt * sn.d.ns;
                 pa = (cw * Un) / NC;
                 pe = ((cw + 1) * Un) / NC;
-                pcu = dn.cu;
-                psrc = dn.idx + (size_t(shn.t0) * dn.ns + pa) * UW;
+                pcu = sn.d.cu;
+                psrc = sn.d.idx + (size_t(sn.t0) * sn.d.ns + pa) * UW;
                 pvalid = true;
             }
             if (pa < pe) {
@@ -398,9 +462,10 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
         }
     };
     for (uint32_t k = 0; k < WS; ++k) issue_next();
-    // dev profile (DSQ_STACK_DBG bit 2): cycles per consumer warp spent
-    // waiting for x / partial buffers, waiting for ring data, decoding, in
-    // the CSR rounds, and at layer boundaries (descriptor + CSR staging waits)
+    // dev profile (build with -DDSQ_STACK_PROFILE, run with DSQ_STACK_DBG bit
+    // 2): cycles per consumer warp spent waiting for x / partial buffers,
+    // waiting for ring data, decoding, and at layer boundaries
+#ifdef DSQ_STACK_PROFILE
     const bool prof = (p.dbg & 4u) && p.trace;
     long long c_xw = 0, c_fw = 0, c_dense = 0, c_csr = 0, c_top = 0, t_mark = clock64();
     auto lap = [&](long long& acc) {
@@ -410,51 +475,33 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
             t_mark = t;
         }
     };
+#define DSQ_LAP(acc) lap(acc)
+#else
+#define DSQ_LAP(acc) \
+    do {             \
+    } while (0)
+#endif
     for (uint32_t l = 0; l < p.n_layers; ++l) {
         const uint32_t b = l & 1u;
-        const StackLayerDesc& d = desc_wait(l).d;
-        const Share sh = cta_share(d, cta);
-        const uint32_t nrows = sh.nrows, NS = d.ns, cu = d.cu;
-        (void)cu;
+        const SDesc& sd = desc_wait(l);
+        const StackLayerDesc& d = sd.d;
+        const uint32_t NS = d.ns, cu = d.cu;
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrConsStart);
-        lap(c_top);
+        DSQ_LAP(c_top);
         mbar_wait(&xfull[b], (l >> 1) & 1u);
         if (l >= 2) mbar_wait(&pempty[b], ((l >> 1) - 1) & 1u);
-        lap(c_xw);
+        DSQ_LAP(c_xw);
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrXReady);
         const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_bytes);
         const uint32_t* luts = reinterpret_cast<const uint32_t*>(sm + p.off_lut + b * p.lut_bytes);
         float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * NC;
-
-        // CSR deltas: rounds distributed over the consumer warps; half of the
-        // warps (alternating per layer) do theirs before the dense units
-        auto csr_phase = [&]() {
-            mbar_wait(&cfull[b], (l >> 1) & 1u);
-            lap(c_top);
-            const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
-            const uint32_t e0 = rp[0], nz = rp[nrows] - e0;
-            const bool staged = nz <= p.csr_cap - 4;
-            const uint32_t* ent = staged ? reinterpret_cast<const uint32_t*>(sm + p.off_csr) +
-                                               b * p.csr_cap + (e0 & 3u)
-                                         : d.csr + e0;
-            const uint32_t* hb = staged ? reinterpret_cast<const uint32_t*>(sm + p.off_hb) + b * p.hb_words
-                                        : d.csr_heads;
-            csr_rounds(e0, nz, ent, hb, staged ? ((e0 >> 5) & ~3u) : 0u, xh,
-                       reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_rounds * 32,
-                       p.gseg + (size_t(cta) * 2 + b) * p.gseg_rounds * 32, p.seg_rounds, cw, NC,
-                       lane);
-            __syncwarp();
-            lap(c_csr);
-        };
-        const bool csr_first = !(p.dbg & 8u) && ((cw + l) & 1u) != 0;
-        if (csr_first) csr_phase();
 
         // dense units: warp cw owns the contiguous unit range [u0, u1) of the
         // CTA share (tile-major: unit u = (tile u / NS, span u % NS)), which
         // its own TMA ring brings in, cu units per chunk.  The accumulators
         // follow the warp across chunks and are flushed into part[cw][row]
         // on a tile change.
-        const uint32_t U = sh.nt * NS;
+        const uint32_t U = sd.nt * NS;
         const uint32_t u0 = (cw * U) / NC, u1 = ((cw + 1) * U) / NC;
         uint32_t cur_tile = 0xffffffffu;
         Planes16 P;
@@ -468,9 +515,9 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
             }
         };
         for (uint32_t cb = u0; cb < u1; cb += cu) {
-            lap(c_dense);
+            DSQ_LAP(c_dense);
             mbar_wait(&full[cw * WS + cslot], cphase);
-            lap(c_fw);
+            DSQ_LAP(c_fw);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(cw * WS + cslot) * p.slot_bytes);
             uint32_t u = cb;
             const uint32_t ue = min(u1, cb + cu);
@@ -545,8 +592,7 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
         }
         flush();
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrDenseDone);
-        lap(c_dense);
-        if (!csr_first) csr_phase();
+        DSQ_LAP(c_dense);
         __syncwarp();
         desc_release(l);
         if (lane == 0) {
@@ -554,6 +600,7 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
             mbar_arrive(&bempty[b]);
         }
     }
+#ifdef DSQ_STACK_PROFILE
     if (prof && lane == 0) {
         long long* o = reinterpret_cast<long long*>(p.trace) + (size_t(cta) * NC + cw) * 5;
         o[0] = c_xw;
@@ -562,12 +609,13 @@ __global__ void __launch_bounds__((NC + 3) * 32, 1) stack_gemv(const __grid_cons
         o[3] = c_csr;
         o[4] = c_top;
     }
+#endif
 }
 
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3((p.consumers + 3) * 32);
+    cfg.blockDim = dim3((p.consumers + 3 + kCsrWarps) * 32);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -575,14 +623,14 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static bool attr_done[6][64] = {};
+    static bool attr_done[4][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    const int ci = p.consumers == 8 ? 0 : p.consumers == 16 ? 1 : 2;
-    const int bi = (p.bits == 3 ? 0 : 1) * 3 + ci;
+    const int ci = p.consumers == 8 ? 0 : 1;
+    const int bi = (p.bits == 3 ? 0 : 1) * 2 + ci;
     using K = void (*)(StackParams);
-    static const K kerns[6] = {stack_gemv<3, 8>, stack_gemv<3, 16>, stack_gemv<3, 24>,
-                               stack_gemv<4, 8>, stack_gemv<4, 16>, stack_gemv<4, 24>};
+    static const K kerns[4] = {stack_gemv<3, 8>, stack_gemv<3, 16>, stack_gemv<4, 8>,
+                               stack_gemv<4, 16>};
     const K kern = kerns[bi];
     if (dev < 0 || dev >= 64 || !attr_done[bi][dev]) {
         int max_optin = 0;

@@ -37,7 +37,7 @@
 
 namespace sqz {
 
-constexpr int kStackConsumersDefault = 16;  // decode warps per CTA (8/16/24; DSQ_STACK_CONSUMERS)
+constexpr int kStackConsumersDefault = 16;  // decode warps per CTA (8/16; DSQ_STACK_CONSUMERS)
 constexpr uint32_t kNoDep = 0xffffffffu;
 constexpr uint32_t kInlineLayers = 8;  // layer descs carried in the launch params
 constexpr uint32_t kTileRows = 4;
@@ -79,8 +79,8 @@ struct StackParams {
     uint32_t n_layers;
     uint32_t bits;
     uint32_t* counters;       // [n_layers + 1] completion counts (self-resetting)
-    float* gseg;              // global spill for CSR round results [G][gseg_rounds][32]
-    uint32_t gseg_rounds;
+    float* gseg;              // global CSR scan results for CTAs beyond csr_cap [G][2][gseg_cap]
+    uint32_t gseg_cap;
     uint32_t grid;            // CTAs (== SMs, all co-resident)
     uint32_t consumers;       // decode warps per CTA (+ producer, loader, finisher warps)
     // dynamic shared memory carve-up (byte offsets)
@@ -92,7 +92,7 @@ struct StackParams {
     uint32_t off_csr, csr_cap;       // two CSR entry buffers (entries)
     uint32_t off_hb, hb_words;       // two row-start bitmap buffers (words)
     uint32_t off_part, part_rows;    // two [consumers][part_rows] dense-partial buffers
-    uint32_t off_seg, seg_rounds;    // CSR round scan results (rounds x 32 floats)
+    uint32_t off_seg, seg_cap;       // two CSR scan-result buffers (floats, position-indexed)
     uint32_t smem_bytes;
     // dev-only experiment switches (DSQ_STACK_DBG): bit 0 skips the decode math
     // (results are garbage; measures the streaming skeleton alone), bit 2

@@ -71,14 +71,31 @@ __device__ __forceinline__ void quad16(uint32_t s, uint32_t pk, const Planes16& 
     p23 = prmt(lo, hi, 0x7362);
 }
 
+// Right shifts on the FMA pipe: k = 2^(32-s) in a register the compiler cannot
+// see through (a kernel argument), so mul.hi stays an IMAD.HI and is not
+// strength-reduced back to an ALU shift.
+struct ShiftK {
+    uint32_t k29, k30, k31;
+};
+
 // one lane's share of one (tile, span), 3-bit: words w0..w2 -> 4 HMMAs into
-// two accumulator sets (breaks the HMMA dependency chain)
+// two accumulator sets (breaks the HMMA dependency chain).  With ShiftK the
+// spare-index gather runs its three shifts as IMAD.HI (FMA pipe).
+template <bool kImadGather = false>
 __device__ __forceinline__ void span3_mma(uint32_t w0, uint32_t w1, uint32_t w2, const Planes8& P,
                                           const uint4& xa, const uint4& xb, float (&d0)[4],
-                                          float (&d1)[4]) {
+                                          float (&d1)[4], ShiftK K = ShiftK{0, 0, 0}) {
     const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
-    const uint32_t t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) |
-                       ((w2 >> 1) & 0x44444444u);
+    uint32_t t;
+    if constexpr (kImadGather) {
+        const uint32_t e0 = w0 & 0x88888888u, e1 = w1 & 0x88888888u, e2 = w2 & 0x88888888u;
+        uint32_t a, b;
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(a) : "r"(e2), "r"(K.k31));
+        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(e1), "r"(K.k30), "r"(a));
+        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(e0), "r"(K.k29), "r"(b));
+    } else {
+        t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) | ((w2 >> 1) & 0x44444444u);
+    }
     const uint32_t sA[4] = {m0, hi16(m0), m1, hi16(m1)};
     const uint32_t sB[4] = {m2, hi16(m2), t, hi16(t)};
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};

@@ -133,6 +133,9 @@ __global__ void __launch_bounds__(768) k_hmma(int niter, float* out, Clk* clk, u
       } else if (VAR == 5) {   // the product's span3_mma (dual accumulators)
         sqz::Planes8 PP{P[r].l0, P[r].l1, P[r].h0, P[r].h1};
         sqz::span3_mma(wp[0], wp[32], wp[64], PP, xa, xb, d[r], d2[r]);
+      } else if (VAR == 6) {   // + IMAD.HI spare-index gather
+        sqz::Planes8 PP{P[r].l0, P[r].l1, P[r].h0, P[r].h1};
+        sqz::span3_mma<true>(wp[0], wp[32], wp[64], PP, xa, xb, d[r], d2[r], sqz::ShiftK{k29, k30, k31});
       } else if (VAR == 3) {
         span3<2>(wp[0], wp[32], wp[64], P[r], xa, xb, d[r], k16, k29, k30, k31);
       } else if (VAR == 4) {
@@ -176,15 +179,12 @@ int main(){
            weights/(ms*1e-3)*bpw/1e9, wpc*nsm*1.965e9*bpw/1e9);
     return 0;
   };
-  for (int warps : {8, 16, 24}) {
-    run(k_hmma<3,1>, "3b HMUL-hi RT1", 3, 1, warps, 1);
-    run(k_hmma<3,1,1>, "3b HMUL-hi RT1 xcf", 3, 1, warps, 1);
-    run(k_hmma<3,2>, "3b HMUL-hi RT2", 3, 2, warps, 1);
-    run(k_hmma<3,2,1>, "3b HMUL-hi RT2 xcf", 3, 2, warps, 1);
-    run(k_hmma<3,4,1>, "3b HMUL-hi RT4 xcf", 3, 4, warps, 1);
+  for (int warps : {8, 12, 16}) {
     run(k_hmma<5,1,1>, "3b product RT1 xcf", 5, 1, warps, 1);
+    run(k_hmma<6,1,1>, "3b product+imad RT1 xcf", 6, 1, warps, 1);
     run(k_hmma<5,2,1>, "3b product RT2 xcf", 5, 2, warps, 1);
-    run(k_hmma<2,2,1>, "4b       RT2 xcf", 2, 2, warps, 1);
+    run(k_hmma<6,2,1>, "3b product+imad RT2 xcf", 6, 2, warps, 1);
+
   }
   return 0;
 }

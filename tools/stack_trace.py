@@ -14,8 +14,8 @@ os.environ["DSQ_STACK_TRACE"] = "1"
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 SLOTS = ["ld_start", "csr_staged", "dep_met", "x_issued", "c_start", "x_ready", "dense_done",
          "csr_done", "signaled", "prod_first", "all_dense", "final_done"]
-SHOW = ["dep_met", "x_issued", "c_start", "x_ready", "dense_done", "all_dense", "final_done",
-        "signaled", "prod_first"]
+SHOW = ["dep_met", "x_issued", "c_start", "x_ready", "dense_done", "csr_staged", "csr_done",
+        "all_dense", "final_done", "signaled"]
 
 
 def main():
