@@ -6,7 +6,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas 
 PKG       := paper_2306_07629_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libdsq_cuda.so
-OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/api.o
+OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/api.o $(CSRC)/container.o
 
 all: $(LIB) oracle cxx-test
 
@@ -18,6 +18,9 @@ $(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layo
 
 $(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/layout.hpp $(CSRC)/stack.hpp include/dsq_cuda.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC,-fopenmp -c $< -o $@
+
+$(CSRC)/container.o: $(CSRC)/container.cpp include/dsq_cuda.h
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -c $< -o $@
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp

@@ -210,6 +210,36 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
 int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
 int dsq_cuda_stack_destroy(dsq_cuda_stack* stack);
 
+/* ---- quantized-model containers ("DSQCONT1") ----------------------------- */
+/* The on-disk input of the hot path: load_container (reference
+ * src/container.cpp:181-223, read_layer :102-142) -- magic, version, CRC-32,
+ * little-endian fields, per-layer QuantizedLayer::validate -- with the same
+ * error codes, then every layer is uploaded (dsq_cuda_layer_create; the fp32
+ * centroids / deltas are rounded to fp16, dsq_layer_info reports exactness). */
+typedef struct dsq_container_meta {
+    uint32_t bits;               /* QuantConfig (container.cpp:150-158)        */
+    double sensitive_fraction;
+    double outlier_fraction;
+    uint32_t group_size;
+    uint32_t kmeans_max_iters;
+    double kmeans_tol;
+    uint64_t seed;
+    uint32_t hybrid_top_k;
+    uint32_t method_code;
+    uint32_t n_layers;
+} dsq_container_meta;
+
+typedef struct dsq_cuda_container dsq_cuda_container;
+/* parse + validate only (host, no device): the reference's load_container
+ * checks, for tools and tests */
+int dsq_container_check(const char* path, dsq_container_meta* meta);
+int dsq_cuda_container_open(const char* path, int device, dsq_cuda_container** out);
+int dsq_cuda_container_meta(const dsq_cuda_container* c, dsq_container_meta* meta);
+/* borrowed handles, valid until dsq_cuda_container_close */
+dsq_cuda_layer* dsq_cuda_container_layer(const dsq_cuda_container* c, uint32_t index);
+const char* dsq_cuda_container_layer_name(const dsq_cuda_container* c, uint32_t index);
+int dsq_cuda_container_close(dsq_cuda_container* c);
+
 #ifdef __cplusplus
 }
 #endif

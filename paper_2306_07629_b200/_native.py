@@ -78,6 +78,15 @@ class LayerInfo(C.Structure):
     ]
 
 
+class ContainerMeta(C.Structure):
+    _fields_ = [
+        ("bits", C.c_uint32), ("sensitive_fraction", C.c_double),
+        ("outlier_fraction", C.c_double), ("group_size", C.c_uint32),
+        ("kmeans_max_iters", C.c_uint32), ("kmeans_tol", C.c_double), ("seed", C.c_uint64),
+        ("hybrid_top_k", C.c_uint32), ("method_code", C.c_uint32), ("n_layers", C.c_uint32),
+    ]
+
+
 # every symbol declared in include/dsq_cuda.h, with its ctypes prototype
 PROTOTYPES = {
     "dsq_cuda_abi_version": (C.c_int, []),
@@ -108,6 +117,12 @@ PROTOTYPES = {
                                         C.POINTER(C.c_void_p)]),
     "dsq_cuda_stack_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_stack_destroy": (C.c_int, [C.c_void_p]),
+    "dsq_container_check": (C.c_int, [C.c_char_p, C.POINTER(ContainerMeta)]),
+    "dsq_cuda_container_open": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "dsq_cuda_container_meta": (C.c_int, [C.c_void_p, C.POINTER(ContainerMeta)]),
+    "dsq_cuda_container_layer": (C.c_void_p, [C.c_void_p, C.c_uint32]),
+    "dsq_cuda_container_layer_name": (C.c_char_p, [C.c_void_p, C.c_uint32]),
+    "dsq_cuda_container_close": (C.c_int, [C.c_void_p]),
 }
 
 

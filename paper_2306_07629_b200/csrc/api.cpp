@@ -303,6 +303,16 @@ struct dsq_cuda_layer {
     std::mutex host_mu;  // serializes the host-buffer API on the internal stream
 };
 
+// shared with container.cpp (C linkage, not in the public header)
+extern "C" int dsq_internal_fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
 extern "C" {
 
 int dsq_cuda_abi_version(void) { return DSQ_CUDA_ABI_VERSION; }
@@ -372,6 +382,8 @@ static int validate_view(const dsq_layer_view* v) {
                     "%s: device path implements channel-wise LUTs (groups_per_row == 1)", v->name);
     return DSQ_OK;
 }
+
+int dsq_internal_validate_view(const dsq_layer_view* v) { return validate_view(v); }
 
 int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** out) {
     if (!out) return fail(DSQ_E_INVALID_ARGUMENT, "null output handle");

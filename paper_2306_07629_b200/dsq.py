@@ -167,6 +167,55 @@ class DeviceLayer:
     def close(self) -> None:
         self._fin()
 
+    @classmethod
+    def _borrowed(cls, handle: C.c_void_p, owner) -> "DeviceLayer":
+        """A view of a layer owned by a DeviceContainer (no finalizer)."""
+        d = cls.__new__(cls)
+        d.handle = handle
+        d._owner = owner
+        i = d.info()
+        d.rows, d.cols = i.rows, i.cols
+        d._fin = lambda: None
+        return d
+
+
+def _meta_dict(m: N.ContainerMeta) -> dict:
+    return {k: getattr(m, k) for k, _ in N.ContainerMeta._fields_}
+
+
+def check_container(path) -> dict:
+    """load_container's checks (reference container.cpp:181-223) on the host:
+    returns the QuantConfig meta or raises DsqError with the reference errc."""
+    m = N.ContainerMeta()
+    check(lib.dsq_container_check(str(path).encode(), C.byref(m)))
+    return _meta_dict(m)
+
+
+class DeviceContainer:
+    """A "DSQCONT1" quantized-model container (reference container.hpp) loaded
+    and uploaded: ``layers`` are device layers in file order, ``names`` their
+    names, ``meta`` the QuantConfig (dsq_cuda_container_open)."""
+
+    def __init__(self, path, device: int = 0):
+        h = C.c_void_p()
+        check(lib.dsq_cuda_container_open(str(path).encode(), device, C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.dsq_cuda_container_close, h)
+        m = N.ContainerMeta()
+        check(lib.dsq_cuda_container_meta(h, C.byref(m)))
+        self.meta = _meta_dict(m)
+        n = m.n_layers
+        self.layers = [DeviceLayer._borrowed(C.c_void_p(lib.dsq_cuda_container_layer(h, i)), self)
+                       for i in range(n)]
+        self.names = [lib.dsq_cuda_container_layer_name(h, i).decode() for i in range(n)]
+
+    def close(self) -> None:
+        self._fin()
+
+
+def load_container(path, device: int = 0) -> DeviceContainer:
+    return DeviceContainer(path, device)
+
 
 class DeviceStack:
     """A dependency chain of uploaded layers run by ONE persistent launch
