@@ -210,6 +210,33 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
 int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
 int dsq_cuda_stack_destroy(dsq_cuda_stack* stack);
 
+/* ---- tensor parallelism: the all-reduce fused into the stack -- */
+/* One context per rank (one process per GPU): a receive buffer for the
+ * partial outputs of row-parallel layers ([2][world][max_rows] fp32) and
+ * per-CTA arrival flags, shared with the peers through CUDA IPC
+ * (ipc_handle_out: 64 bytes, cudaIpcMemHandle_t; exchange them with any
+ * out-of-band channel, e.g. torch.distributed all_gather, then
+ * dsq_cuda_tp_connect with all world handles in rank order).  No reference
+ * counterpart (the reference is single-process). */
+typedef struct dsq_cuda_tp dsq_cuda_tp;
+int dsq_cuda_tp_create(int device, uint32_t world, uint32_t rank, uint32_t max_rows,
+                       uint32_t max_grid, dsq_cuda_tp** out, void* ipc_handle_out);
+int dsq_cuda_tp_connect(dsq_cuda_tp* tp, const void* handles);
+/* single-process: contexts of one process (same or P2P-capable devices) */
+int dsq_cuda_tp_connect_local(dsq_cuda_tp* const* ctxs, uint32_t world);
+int dsq_cuda_tp_destroy(dsq_cuda_tp* tp);
+/* A stack whose layers with reduce[i] != 0 produce partial sums (row-parallel
+ * shards): the finishing CTAs write their partial rows to every rank's
+ * receive buffer over NVLink peer memory, signal the same CTA index on every
+ * rank (release, system scope), wait for all ranks, and store the sum in rank
+ * order as y_i -- no NCCL call and no extra launch on the data path.  All
+ * ranks must create the same stacks (same grid) and run them in the same
+ * order.  grid = CTAs (0: one per SM). */
+int dsq_cuda_stack_create_tp(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                             const void* const* xs, void* const* ys, int y_dtype,
+                             const uint8_t* reduce, dsq_cuda_tp* tp, uint32_t grid,
+                             dsq_cuda_stack** out);
+
 /* ---- quantized-model containers ("DSQCONT1") ----------------------------- */
 /* The on-disk input of the hot path: load_container (reference
  * src/container.cpp:181-223, read_layer :102-142) -- magic, version, CRC-32,

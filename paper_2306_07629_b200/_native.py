@@ -117,6 +117,15 @@ PROTOTYPES = {
                                         C.POINTER(C.c_void_p)]),
     "dsq_cuda_stack_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_stack_destroy": (C.c_int, [C.c_void_p]),
+    "dsq_cuda_tp_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.POINTER(C.c_void_p), C.c_void_p]),
+    "dsq_cuda_tp_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dsq_cuda_tp_connect_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32]),
+    "dsq_cuda_tp_destroy": (C.c_int, [C.c_void_p]),
+    "dsq_cuda_stack_create_tp": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32,
+                                           C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                                           C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_void_p,
+                                           C.c_uint32, C.POINTER(C.c_void_p)]),
     "dsq_container_check": (C.c_int, [C.c_char_p, C.POINTER(ContainerMeta)]),
     "dsq_cuda_container_open": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     "dsq_cuda_container_meta": (C.c_int, [C.c_void_p, C.POINTER(ContainerMeta)]),

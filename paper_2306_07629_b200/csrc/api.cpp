@@ -200,6 +200,7 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, 
     d.ns = l.ns;
     d.cu = slot_bytes / (unit_words(bits) * 4);
     d.dep = kNoDep;
+    d.reduce_ord = kNoDep;
     d.nch_lo = ceil_div(uint64_t(d.tq) * l.ns, d.cu);
     d.nch_hi = ceil_div(uint64_t(d.tq + 1) * l.ns, d.cu);
 }
@@ -852,17 +853,30 @@ int dsq_cuda_dequant(const dsq_cuda_layer* L, void* w_dev, int out_dtype, void* 
     return DSQ_OK;
 }
 
+struct dsq_cuda_tp {
+    int device = 0;
+    uint32_t world = 1, rank = 0, max_rows = 0, max_grid = 0;
+    void* buf = nullptr;           // recv [2][world][max_rows] fp32 + flags [max_grid] u32
+    size_t recv_bytes = 0;
+    uint64_t base = 0;             // reduce ordinals completed by earlier launches
+    void* peer_base[8] = {};       // mapped peer buffers (own: buf)
+    bool peer_ipc[8] = {};
+};
+
 struct dsq_cuda_stack {
     int device = 0;
     uint32_t n = 0;
+    uint32_t n_reduce = 0;
+    dsq_cuda_tp* tp = nullptr;
     StackParams sp{};
     void* arena = nullptr;
     unsigned long long* trace = nullptr;  // DSQ_STACK_TRACE=1: per-CTA layer timeline
 };
 
-int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
-                          const void* const* xs, void* const* ys, int y_dtype,
-                          dsq_cuda_stack** out) {
+static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                             const void* const* xs, void* const* ys, int y_dtype,
+                             const uint8_t* reduce, dsq_cuda_tp* tp, uint32_t grid,
+                             dsq_cuda_stack** out) {
     if (!out || !layers || !deps || !xs || !ys || n == 0)
         return fail(DSQ_E_INVALID_ARGUMENT, "stack: null argument or empty stack");
     *out = nullptr;
@@ -870,13 +884,19 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
         return fail(DSQ_E_INVALID_ARGUMENT, "stack: y dtype must be F32 or F16");
     const dsq_cuda_layer* L0 = layers[0];
     if (!L0) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null layer");
+    const int G = grid ? int(grid) : L0->num_sms;
+    if (G < 1 || G > L0->num_sms)
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack: grid must be 1..%d CTAs", L0->num_sms);
+    if (tp && (tp->device != L0->device || uint32_t(G) > tp->max_grid))
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack: TP context device / grid mismatch");
     std::vector<StackPlanLayer> pl(n);
+    uint32_t n_reduce = 0;
     for (uint32_t i = 0; i < n; ++i) {
         const dsq_cuda_layer* L = layers[i];
         if (!L) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null layer %u", i);
         if (!L->rec_layout || L->bits != L0->bits)
             return fail(DSQ_E_UNSUPPORTED, "stack: layers must all be 3-bit or all 4-bit");
-        if (L->device != L0->device || L->num_sms != L0->num_sms)
+        if (L->device != L0->device)
             return fail(DSQ_E_INVALID_ARGUMENT, "stack: layers on different devices");
         if (deps[i] >= 0) {
             if (uint32_t(deps[i]) >= i)
@@ -889,58 +909,97 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
             return fail(DSQ_E_INVALID_ARGUMENT, "stack: x %u must be a 16-byte aligned fp16 buffer", i);
         }
         if (!ys[i]) return fail(DSQ_E_INVALID_ARGUMENT, "stack: null y %u", i);
+        if (reduce && reduce[i]) {
+            if (!tp) return fail(DSQ_E_INVALID_ARGUMENT, "stack: reduce layer %u without TP context", i);
+            if (L->rows > tp->max_rows)
+                return fail(DSQ_E_SHAPE_MISMATCH, "stack: reduce layer %u rows > TP max_rows", i);
+            ++n_reduce;
+        }
         pl[i] = StackPlanLayer{L->rows, L->cols, L->tiles, L->ns,
-                               max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
+                               max_nnz_per_cta(L->row_ptr_host, L->rows, G)};
     }
     CUDA_TRY(cudaSetDevice(L0->device));
     auto* S = new dsq_cuda_stack;
     S->device = L0->device;
     S->n = n;
+    S->n_reduce = n_reduce;
+    S->tp = tp;
     uint32_t gseg_cap = 0;
-    int rc = plan_stack(pl.data(), n, L0->num_sms, L0->bits, S->sp, gseg_cap);
+    int rc = plan_stack(pl.data(), n, G, L0->bits, S->sp, gseg_cap);
     if (rc) {
         delete S;
         return rc;
     }
+    // per-(layer, CTA) CSR entry ranges for this grid
+    std::vector<uint32_t> rng(size_t(n) * G * 2);
+    for (uint32_t i = 0; i < n; ++i) {
+        const dsq_cuda_layer* L = layers[i];
+        for (int c = 0; c < G; ++c) {
+            uint32_t t0, nt;
+            tile_share(L->tiles, G, uint32_t(c), t0, nt);
+            const uint32_t r0 = std::min(t0 * kTileRows, L->rows);
+            const uint32_t r1 = std::min((t0 + nt) * kTileRows, L->rows);
+            rng[(size_t(i) * G + c) * 2] = L->row_ptr_host[r0];
+            rng[(size_t(i) * G + c) * 2 + 1] = L->row_ptr_host[r1];
+        }
+    }
+    const size_t tb = (size_t(n) * sizeof(StackLayerDesc) + 255) & ~size_t(255);
+    const size_t cb = ((size_t(n) + 1) * 4 + 255) & ~size_t(255);
+    const size_t rb = (rng.size() * 4 + 255) & ~size_t(255);
+    const size_t gb = size_t(G) * 2 * gseg_cap * 4 + 4;
+    cudaError_t e = cudaMalloc(&S->arena, tb + cb + rb + gb);
+    if (e != cudaSuccess) {
+        delete S;
+        return cuda_fail(e, "cudaMalloc(stack)");
+    }
+    uint8_t* base = static_cast<uint8_t*>(S->arena);
+    const uint32_t* drng = reinterpret_cast<const uint32_t*>(base + tb + cb);
     std::vector<StackLayerDesc> descs(n);
+    uint32_t ord = 0;
     for (uint32_t i = 0; i < n; ++i) {
         StackLayerDesc& d = descs[i];
-        fill_desc(d, pl[i], S->sp.slot_bytes, L0->bits, L0->num_sms);
+        fill_desc(d, pl[i], S->sp.slot_bytes, L0->bits, G);
         const dsq_cuda_layer* L = layers[i];
         d.idx = L->rec;
         d.lut = L->tlut;
         d.row_ptr = L->P.row_ptr;
         d.csr = L->P.csr;
-        d.csr_rng = L->csr_rng;
+        d.csr_rng = drng + size_t(i) * G * 2;
         d.csr_heads = L->csr_heads;
         d.dep = deps[i] >= 0 ? uint32_t(deps[i]) : kNoDep;
         d.x = deps[i] >= 0 ? static_cast<const uint16_t*>(ys[deps[i]])
                            : static_cast<const uint16_t*>(xs[i]);
         d.y = ys[i];
         d.y_f16 = y_dtype == DSQ_F16 ? 1u : 0u;
+        d.reduce_ord = (reduce && reduce[i]) ? ord++ : kNoDep;
         if (i < kInlineLayers) S->sp.inl[i] = d;
     }
-    const size_t tb = (size_t(n) * sizeof(StackLayerDesc) + 255) & ~size_t(255);
-    const size_t cb = ((size_t(n) + 1) * 4 + 255) & ~size_t(255);
-    const size_t gb = size_t(L0->num_sms) * 2 * gseg_cap * 4 + 4;
-    cudaError_t e = cudaMalloc(&S->arena, tb + cb + gb);
-    if (e != cudaSuccess) {
-        delete S;
-        return cuda_fail(e, "cudaMalloc(stack)");
-    }
-    uint8_t* base = static_cast<uint8_t*>(S->arena);
     if ((e = cudaMemcpy(base, descs.data(), n * sizeof(StackLayerDesc), cudaMemcpyHostToDevice)) !=
             cudaSuccess ||
-        (e = cudaMemset(base + tb, 0, cb)) != cudaSuccess) {
+        (e = cudaMemset(base + tb, 0, cb)) != cudaSuccess ||
+        (e = cudaMemcpy(base + tb + cb, rng.data(), rng.size() * 4, cudaMemcpyHostToDevice)) !=
+            cudaSuccess) {
         cudaFree(S->arena);
         delete S;
         return cuda_fail(e, "stack upload");
     }
     S->sp.layers = reinterpret_cast<const StackLayerDesc*>(base);
     S->sp.counters = reinterpret_cast<uint32_t*>(base + tb);
-    S->sp.gseg = reinterpret_cast<float*>(base + tb + cb);
+    S->sp.gseg = reinterpret_cast<float*>(base + tb + cb + rb);
     S->sp.gseg_cap = gseg_cap;
     S->sp.n_layers = n;
+    S->sp.tp_world = tp ? tp->world : 1;
+    S->sp.tp_rank = tp ? tp->rank : 0;
+    S->sp.tp_max_rows = tp ? tp->max_rows : 0;
+    if (tp) {
+        S->sp.tp_recv = static_cast<float*>(tp->buf);
+        S->sp.tp_flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(tp->buf) + tp->recv_bytes);
+        for (uint32_t k = 0; k < tp->world; ++k) {
+            S->sp.tp_peer_recv[k] = static_cast<float*>(tp->peer_base[k]);
+            S->sp.tp_peer_flags[k] = reinterpret_cast<uint32_t*>(
+                static_cast<uint8_t*>(tp->peer_base[k]) + tp->recv_bytes);
+        }
+    }
     S->sp.trace = nullptr;
     S->sp.dbg = 0;
     if (const char* t = std::getenv("DSQ_STACK_DBG")) S->sp.dbg = uint32_t(atoi(t));
@@ -955,6 +1014,86 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
         }
     }
     *out = S;
+    return DSQ_OK;
+}
+
+int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                          const void* const* xs, void* const* ys, int y_dtype,
+                          dsq_cuda_stack** out) {
+    return stack_create_impl(layers, n, deps, xs, ys, y_dtype, nullptr, nullptr, 0, out);
+}
+
+int dsq_cuda_stack_create_tp(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                             const void* const* xs, void* const* ys, int y_dtype,
+                             const uint8_t* reduce, dsq_cuda_tp* tp, uint32_t grid,
+                             dsq_cuda_stack** out) {
+    return stack_create_impl(layers, n, deps, xs, ys, y_dtype, reduce, tp, grid, out);
+}
+
+// ---- tensor-parallel context: this rank's receive buffer + flags, peers mapped
+int dsq_cuda_tp_create(int device, uint32_t world, uint32_t rank, uint32_t max_rows,
+                       uint32_t max_grid, dsq_cuda_tp** out, void* ipc_handle) {
+    if (!out || world < 1 || world > 8 || rank >= world || max_rows == 0 || max_grid == 0)
+        return fail(DSQ_E_INVALID_ARGUMENT, "tp: world 1..8, rank < world, sizes > 0");
+    *out = nullptr;
+    CUDA_TRY(cudaSetDevice(device));
+    auto* t = new dsq_cuda_tp;
+    t->device = device;
+    t->world = world;
+    t->rank = rank;
+    t->max_rows = (max_rows + 3) & ~3u;
+    t->max_grid = max_grid;
+    t->recv_bytes = size_t(2) * world * t->max_rows * 4;
+    const size_t bytes = t->recv_bytes + size_t(max_grid) * 4;
+    cudaError_t e = cudaMalloc(&t->buf, bytes);
+    if (e == cudaSuccess) e = cudaMemset(t->buf, 0, bytes);
+    if (e == cudaSuccess && ipc_handle) {
+        cudaIpcMemHandle_t h;
+        e = cudaIpcGetMemHandle(&h, t->buf);
+        if (e == cudaSuccess) std::memcpy(ipc_handle, &h, sizeof(h));
+    }
+    if (e != cudaSuccess) {
+        if (t->buf) cudaFree(t->buf);
+        delete t;
+        return cuda_fail(e, "tp buffer");
+    }
+    t->peer_base[rank] = t->buf;
+    *out = t;
+    return DSQ_OK;
+}
+
+int dsq_cuda_tp_connect(dsq_cuda_tp* t, const void* handles) {
+    if (!t || !handles) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    CUDA_TRY(cudaSetDevice(t->device));
+    for (uint32_t k = 0; k < t->world; ++k) {
+        if (k == t->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t*>(handles) + k * sizeof(h), sizeof(h));
+        void* p = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        t->peer_base[k] = p;
+        t->peer_ipc[k] = true;
+    }
+    return DSQ_OK;
+}
+
+int dsq_cuda_tp_connect_local(dsq_cuda_tp* const* ctxs, uint32_t world) {
+    if (!ctxs || world < 1 || world > 8) return fail(DSQ_E_INVALID_ARGUMENT, "bad contexts");
+    for (uint32_t r = 0; r < world; ++r) {
+        if (!ctxs[r] || ctxs[r]->world != world || ctxs[r]->rank != r)
+            return fail(DSQ_E_INVALID_ARGUMENT, "tp: context %u has the wrong world/rank", r);
+        for (uint32_t k = 0; k < world; ++k) ctxs[r]->peer_base[k] = ctxs[k]->buf;
+    }
+    return DSQ_OK;
+}
+
+int dsq_cuda_tp_destroy(dsq_cuda_tp* t) {
+    if (!t) return DSQ_OK;
+    cudaSetDevice(t->device);
+    for (uint32_t k = 0; k < t->world; ++k)
+        if (t->peer_ipc[k]) cudaIpcCloseMemHandle(t->peer_base[k]);
+    if (t->buf) cudaFree(t->buf);
+    delete t;
     return DSQ_OK;
 }
 
@@ -974,6 +1113,12 @@ extern "C" uint64_t dsq_cuda_stack_trace(dsq_cuda_stack* S, unsigned long long* 
 int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
     if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
     cudaSetDevice(S->device);
+    if (S->tp) {
+        // every rank runs the same sequence of launches, so the reduce
+        // ordinals (and the peers' flag targets) stay in step
+        S->sp.tp_base = uint32_t(S->tp->base);
+        S->tp->base += S->n_reduce;
+    }
     CUDA_TRY(launch_stack(S->sp, static_cast<cudaStream_t>(stream), true));
     return DSQ_OK;
 }

@@ -326,6 +326,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                              ? reinterpret_cast<const float*>(sm + p.off_seg) + size_t(b) * p.seg_cap
                              : p.gseg + (size_t(cta) * 2 + b) * p.gseg_cap;
         float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * NC;
+        const bool tp = d.reduce_ord != kNoDep;
+        const uint32_t par = tp ? (p.tp_base + d.reduce_ord) & 1u : 0u;
         for (uint32_t i = 32 * f + lane; i < sh.nt * kTileRows; i += 32 * kFin) {
             float s = 0.f;
 #pragma unroll
@@ -337,10 +339,38 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             const uint32_t a = rp[i] - ea, e = rp[i + 1] - ea;
             for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j)
                 s += S[j * 128 + min(e - 1 - j * 128, 127u)];
-            if (d.y_f16)
+            if (tp) {
+                // a partial sum: hand it to every rank (own included) at
+                // slot [parity][this rank][row]
+                for (uint32_t k = 0; k < p.tp_world; ++k)
+                    p.tp_peer_recv[k][(size_t(par) * p.tp_world + p.tp_rank) * p.tp_max_rows +
+                                      r0 + i] = s;
+            } else if (d.y_f16) {
                 static_cast<__half*>(d.y)[r0 + i] = __float2half_rn(s);
-            else
+            } else {
                 static_cast<float*>(d.y)[r0 + i] = s;
+            }
+        }
+        if (tp) {
+            // signal the same CTA index on every rank, wait for all ranks'
+            // partials of these rows, then sum them in rank order
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_system();
+                for (uint32_t k = 0; k < p.tp_world; ++k)
+                    red_release_sys_add(p.tp_peer_flags[k] + cta, 1u);
+            }
+            const uint32_t target = (p.tp_base + d.reduce_ord + 1) * p.tp_world * kFin;
+            while (ld_acquire_sys(p.tp_flags + cta) < target) __nanosleep(32);
+            const float* recv = p.tp_recv + size_t(par) * p.tp_world * p.tp_max_rows;
+            for (uint32_t i = 32 * f + lane; i < nrows; i += 32 * kFin) {
+                float s = 0.f;
+                for (uint32_t k = 0; k < p.tp_world; ++k) s += recv[k * p.tp_max_rows + r0 + i];
+                if (d.y_f16)
+                    static_cast<__half*>(d.y)[r0 + i] = __float2half_rn(s);
+                else
+                    static_cast<float*>(d.y)[r0 + i] = s;
+            }
         }
         __syncwarp();
         if (lane == 0) {

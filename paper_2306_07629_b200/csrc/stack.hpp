@@ -67,6 +67,8 @@ struct StackLayerDesc {
     uint32_t tiles, ns;         // ceil(rows/4), ceil(cols/256)
     uint32_t dep;               // layer whose output is x (kNoDep: external input)
     uint32_t y_f16;
+    uint32_t reduce_ord;        // TP: ordinal of this layer among the launch's partial-sum
+                                // (row-parallel) layers, kNoDep if its y is final
     // host-precomputed tile split over the grid (no device division):
     // CTA c owns tiles [c*tq + min(c, tr), ...) -- tq or tq+1 tiles -- whose
     // units are streamed in chunks of cu units (nch_lo / nch_hi chunks)
@@ -94,6 +96,16 @@ struct StackParams {
     uint32_t off_part, part_rows;    // two [consumers][part_rows] dense-partial buffers
     uint32_t off_seg, seg_cap;       // two CSR scan-result buffers (floats, position-indexed)
     uint32_t smem_bytes;
+    // tensor parallelism (world > 1): the partial y of a reduce layer is
+    // summed over the ranks' CTAs with the same index over peer memory.
+    // recv = [2 parities][world][max_rows] fp32 per rank, flags = [grid] u32
+    // monotonic arrival counts per rank; peer_* are the (P2P-mapped) buffers
+    // of every rank, own rank included.
+    uint32_t tp_world, tp_rank, tp_base, tp_max_rows;
+    float* tp_recv;
+    uint32_t* tp_flags;
+    float* tp_peer_recv[8];
+    uint32_t* tp_peer_flags[8];
     // dev-only experiment switches (DSQ_STACK_DBG): bit 0 skips the decode math
     // (results are garbage; measures the streaming skeleton alone), bit 2
     // records the consumer cycle profile into `trace`

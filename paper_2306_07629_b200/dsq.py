@@ -217,20 +217,56 @@ def load_container(path, device: int = 0) -> DeviceContainer:
     return DeviceContainer(path, device)
 
 
+class TPContext:
+    """One rank's tensor-parallel context (dsq_cuda_tp_create): receive buffer
+    + per-CTA flags for the fused all-reduce.  ``ipc_handle`` (64 bytes) goes
+    to the peers; ``connect(handles)`` maps theirs (all ranks, rank order)."""
+
+    def __init__(self, world: int, rank: int, max_rows: int, max_grid: int = 1024,
+                 device: int = 0):
+        h = C.c_void_p()
+        self._ipc = C.create_string_buffer(64)
+        check(lib.dsq_cuda_tp_create(device, world, rank, max_rows, max_grid, C.byref(h),
+                                     self._ipc))
+        self.handle, self.world, self.rank = h, world, rank
+        self.ipc_handle = bytes(self._ipc.raw)
+        self._fin = weakref.finalize(self, lib.dsq_cuda_tp_destroy, h)
+
+    def connect(self, handles: list) -> None:
+        blob = b"".join(handles)
+        check(lib.dsq_cuda_tp_connect(self.handle, blob))
+
+    @staticmethod
+    def connect_local(ctxs: list) -> None:
+        arr = (C.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+        check(lib.dsq_cuda_tp_connect_local(arr, len(ctxs)))
+
+
 class DeviceStack:
     """A dependency chain of uploaded layers run by ONE persistent launch
     (dsq_cuda_stack_create/run).  deps[i] = index of the layer whose output
-    is layer i's x, or -1 for the external fp16 buffer xs[i] (device pointer)."""
+    is layer i's x, or -1 for the external fp16 buffer xs[i] (device pointer).
+    With ``tp`` (a TPContext), layers with reduce[i] produce partial sums that
+    the kernel all-reduces over the ranks' peer memory (dsq_cuda_stack_create_tp);
+    ``grid`` = CTAs (0: one per SM)."""
 
-    def __init__(self, layers: list, deps: list, xs: list, ys: list, y_dtype: int):
+    def __init__(self, layers: list, deps: list, xs: list, ys: list, y_dtype: int,
+                 reduce: list | None = None, tp: "TPContext | None" = None, grid: int = 0):
         n = len(layers)
         self._layers = list(layers)  # keep the layer handles alive
+        self._tp = tp
         arr_l = (C.c_void_p * n)(*[d.handle.value for d in layers])
         arr_d = (C.c_int32 * n)(*deps)
         arr_x = (C.c_void_p * n)(*[x or 0 for x in xs])
         arr_y = (C.c_void_p * n)(*ys)
         h = C.c_void_p()
-        check(lib.dsq_cuda_stack_create(arr_l, n, arr_d, arr_x, arr_y, y_dtype, C.byref(h)))
+        if tp is None and reduce is None and grid == 0:
+            check(lib.dsq_cuda_stack_create(arr_l, n, arr_d, arr_x, arr_y, y_dtype, C.byref(h)))
+        else:
+            red = (C.c_uint8 * n)(*([1 if r else 0 for r in reduce] if reduce else [0] * n))
+            check(lib.dsq_cuda_stack_create_tp(arr_l, n, arr_d, arr_x, arr_y, y_dtype, red,
+                                               tp.handle if tp is not None else None, grid,
+                                               C.byref(h)))
         self.handle = h
         self._fin = weakref.finalize(self, lib.dsq_cuda_stack_destroy, h)
 

@@ -54,10 +54,11 @@ def _pack_rows(idx: np.ndarray, bits: int) -> np.ndarray:
     return np.packbits(b, axis=1, bitorder="little").reshape(-1)
 
 
-def shard_rows(layer: QuantizedLayer, rank: int, world: int) -> tuple[QuantizedLayer, int, int]:
+def shard_rows(layer: QuantizedLayer, rank: int, world: int,
+               align: int = 1) -> tuple[QuantizedLayer, int, int]:
     """Column-parallel shard: output rows [r0, r1)."""
     p, s = layer.packed, layer.sparse
-    r0, r1 = split_range(layer.rows, world, rank)
+    r0, r1 = split_range(layer.rows, world, rank, align)
     k = p.levels() * p.groups_per_row
     stride = p.row_stride()
     a, b = int(s.row_ptr[r0]), int(s.row_ptr[r1])
@@ -90,3 +91,49 @@ def shard_cols(layer: QuantizedLayer, rank: int, world: int,
                        np.asarray(s.values)[keep])
     return (QuantizedLayer(f"{layer.name}.c{rank}", layer.rows, c1 - c0, packed, sparse,
                            layer.hybrid_top_k), c0, c1)
+
+
+# ---------------------------------------------------------------------------
+# decoder-layer tensor parallelism (Megatron-style), the fused-reduce stack
+# ---------------------------------------------------------------------------
+# v,q,k,o,up,gate,down: column-parallel (rows split) for v,q,k,up,gate,
+# row-parallel (cols split, partial sums reduced) for o and down.  The row
+# split of a producer equals the column split of its consumer (same 32-aligned
+# split_range), so o reads v's local slice and down reads up's local slice
+# with no exchange; the two reduces per decoder layer run inside the kernel.
+DECODER = ["v", "q", "k", "o", "up", "gate", "down"]
+ROW_PARALLEL = {"o", "down"}
+CHAIN_IN = [-1, -1, -1, 0, 3, 3, 4]  # input of each GEMV within a step (bench.py)
+
+
+def shard_decoder(layers: list, rank: int, world: int, align: int = 32) -> list:
+    """The 7 shards (QuantizedLayer) of one decoder layer for `rank`."""
+    out = []
+    for name, q in zip(DECODER, layers):
+        if world == 1:
+            out.append(q)
+        elif name in ROW_PARALLEL:
+            out.append(shard_cols(q, rank, world, align)[0])
+        else:
+            out.append(shard_rows(q, rank, world, align)[0])
+    return out
+
+
+def decoder_chain(n_steps: int, slots: int, first_x: bool = True):
+    """deps / reduce flags of n_steps chained decoder layers (7 GEMVs each):
+    v,q,k read the step input (the previous step's reduced down output, or
+    the external x for the first step), o <- v, up,gate <- o, down <- up.
+    Returns (deps, reduce, slot_of_gemv)."""
+    deps, reduce, slot = [], [], []
+    prev_down = -1
+    for s in range(n_steps):
+        base = len(deps)
+        for j, name in enumerate(DECODER):
+            if CHAIN_IN[j] < 0:
+                deps.append(prev_down if (prev_down >= 0 or not first_x) else -1)
+            else:
+                deps.append(base + CHAIN_IN[j])
+            reduce.append(name in ROW_PARALLEL)
+            slot.append(s % slots)
+        prev_down = base + len(DECODER) - 1
+    return deps, reduce, slot

@@ -32,3 +32,11 @@ def reference():
     if not REF_SO.exists():
         pytest.skip("oracle/_ref not built")
     return Reference()
+
+
+@pytest.fixture(scope="session")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
