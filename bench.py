@@ -429,6 +429,152 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     print(json.dumps(line), flush=True)
 
 
+class TPUnavailable(RuntimeError):
+    pass
+
+
+def run_ours_tp(args, rank: int, world: int, local_rank: int):
+    """N GPUs, one decoder-layer chain tensor-parallel over all of them
+    (Megatron split: v,q,k,up,gate column-parallel, o,down row-parallel),
+    the two all-reduces per decoder layer fused into the persistent stack
+    kernel over NVLink peer memory (CUDA IPC-mapped receive buffers, per-CTA
+    release/acquire flags at system scope).  value = the whole model's
+    reference-charged bytes per step / step time (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2306_07629_b200._native as N
+    from paper_2306_07629_b200 import DeviceLayer, DeviceStack
+    from paper_2306_07629_b200.dsq import TPContext
+    from paper_2306_07629_b200.tp import decoder_chain, shard_decoder
+    from oracle.oracle import make_x, to_quantized_layer
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    t_setup = time.time()
+    host_layers = build_host_layers()
+    qls = [to_quantized_layer(L, name=n) for L, (n, _, _) in zip(host_layers, SHAPES)]
+    bytes_step = sum(int(N.lib.dsq_bytes_touched_estimate(r, c, BITS, 0, L.nnz))
+                     for L, (_, r, c) in zip(host_layers, SHAPES))
+    shards = shard_decoder(qls, rank, world)
+    n_rot = args.rotation
+    dls = [[DeviceLayer(q, device=local_rank) for q in shards] for _ in range(n_rot)]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ctx = TPContext(world, rank, max_rows=max(r for _, r, _ in SHAPES), max_grid=sms,
+                    device=local_rank)
+    handles = [None] * world
+    dist.all_gather_object(handles, ctx.ipc_handle)
+    ok = 1
+    try:
+        ctx.connect(handles)
+    except Exception as e:  # P2P / IPC unavailable: every rank falls back together
+        print(f"rank {rank}: tp connect failed: {e}", file=sys.stderr)
+        ok = 0
+    flag = torch.tensor([ok], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if not int(flag.item()):
+        raise TPUnavailable("CUDA IPC peer mapping failed")
+    st = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(st)
+    sp = st.cuda_stream
+    x = torch.from_numpy(make_x(4096, seed=100).view(np.int16)).to(dev)
+    ys = [[torch.empty(q.rows, dtype=torch.int16, device=dev) for q in shards]
+          for _ in range(n_rot)]
+
+    def build(nsteps, offset):
+        deps, reduce, _ = decoder_chain(nsteps, 1)
+        layers, yp = [], []
+        for s in range(nsteps):
+            slot = (offset + s) % n_rot
+            layers += dls[slot]
+            yp += [y.data_ptr() for y in ys[slot]]
+        xp = [x.data_ptr() if d < 0 else 0 for d in deps]
+        return DeviceStack(layers, deps, xp, yp, N.F16, reduce=reduce, tp=ctx)
+
+    s_warm, s_time = build(args.warmup, 0), build(args.steps, args.warmup)
+    # every rank runs the same launch sequence (the reduce flag targets
+    # advance per launch): fixed counts, no time-based loops
+    for _ in range(2):
+        s_warm.run(sp)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    for _ in range(max(1, int(args.soak * 20))):
+        s_warm.run(sp)
+    torch.cuda.synchronize()
+    s_warm.run(sp)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    s_time.run(sp)
+    e1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = sampler.stop()
+    ctx.check()
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = bytes_step * args.steps / (ms * 1e-3) / 1e9
+
+    # e2e: one-step TP stacks from host memory (x H2D, step output D2H)
+    e2e = None
+    if not args.no_e2e:
+        one = [build(1, slot) for slot in range(n_rot)]
+        x_host = torch.from_numpy(make_x(4096, seed=7).view(np.int16)).pin_memory()
+        y_host = torch.empty(shards[-1].rows, dtype=torch.int16).pin_memory()
+
+        def step(slot):
+            x.copy_(x_host, non_blocking=True)
+            one[slot].run(sp)
+            y_host.copy_(ys[slot][-1], non_blocking=True)
+            st.synchronize()
+
+        for s in range(3):
+            step(s % n_rot)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(args.e2e_steps):
+            step(s % n_rot)
+        el = time.perf_counter() - t0
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+        ctx.check()
+        e2e = {"value": round(bytes_step * args.e2e_steps / el / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": shards[-1].rows * 2,
+               "steps": args.e2e_steps, "ms_per_step": round(el / args.e2e_steps * 1e3, 4),
+               "api": "DeviceStack.run (dsq_cuda_stack_create_tp) per decoder-layer step on "
+                      "every rank, pinned host x -> device, step output -> host"}
+    if rank != 0:
+        return
+    pk = peaks()
+    peak = float(pk.get("hbm_gbs", 6650.0))
+    per_gpu = value / world
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic (random fp16 centroids/indices/deltas; weights random-init)",
+        "config": workload_config(n_rot, f"tp{world} (fused all-reduce over NVLink peer memory)"),
+        "us_per_layer": round(ms_step * 1e3 / len(SHAPES), 3),
+        "decode_tok_s_linear": round(1e3 / (ms_step * LLAMA7B_LAYERS), 1),
+        "frac_of_8TBs": round(per_gpu / 8000.0, 4),
+        "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(per_gpu / peak, 4), "traffic": None,
+                     "kernel": "sqz::stack_gemv<3> (persistent, fused TP reduce)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback",
+                     "algorithmic_bytes_per_step": bytes_step, "per": "GPU"},
+        "e2e": e2e, "clocks": clocks, "gpu_launches": 1, "gemvs_timed": args.steps * len(SHAPES),
+        "mode": "stack-tp", "setup_s": round(setup_s, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -441,6 +587,10 @@ def main():
     ap.add_argument("--rotation", type=int, default=16,
                     help="decoder layers of distinct device weights (working set >> L2)")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of load before timing")
+    ap.add_argument("--multi", choices=["tp", "replicas"], default="tp",
+                    help="N>1: tensor-parallel decoder layers (fused all-reduce) or N replicas")
+    ap.add_argument("--force-tp", action="store_true",
+                    help="dev: run the TP path even at N=1 (under torchrun)")
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -455,15 +605,24 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
-    if world > 1:
+    use_tp = (world > 1 and args.multi == "tp") or args.force_tp
+    if world > 1 or args.force_tp:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if use_tp:
+            try:
+                run_ours_tp(args, rank, world, local_rank)
+                return
+            except TPUnavailable as e:
+                if rank == 0:
+                    print(f"tensor parallelism unavailable ({e}); running replicas",
+                          file=sys.stderr)
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or args.force_tp:
             import torch.distributed as dist
             dist.destroy_process_group()
 

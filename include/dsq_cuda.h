@@ -224,6 +224,9 @@ int dsq_cuda_tp_create(int device, uint32_t world, uint32_t rank, uint32_t max_r
 int dsq_cuda_tp_connect(dsq_cuda_tp* tp, const void* handles);
 /* single-process: contexts of one process (same or P2P-capable devices) */
 int dsq_cuda_tp_connect_local(dsq_cuda_tp* const* ctxs, uint32_t world);
+/* DSQ_OK, or DSQ_E_INTERNAL if a fused reduce gave up waiting for a peer
+ * (~4 s watchdog: ranks must run the same launch sequence) */
+int dsq_cuda_tp_error(const dsq_cuda_tp* tp);
 int dsq_cuda_tp_destroy(dsq_cuda_tp* tp);
 /* A stack whose layers with reduce[i] != 0 produce partial sums (row-parallel
  * shards): the finishing CTAs write their partial rows to every rank's

@@ -121,6 +121,7 @@ PROTOTYPES = {
                                      C.POINTER(C.c_void_p), C.c_void_p]),
     "dsq_cuda_tp_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_tp_connect_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32]),
+    "dsq_cuda_tp_error": (C.c_int, [C.c_void_p]),
     "dsq_cuda_tp_destroy": (C.c_int, [C.c_void_p]),
     "dsq_cuda_stack_create_tp": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32,
                                            C.POINTER(C.c_int32), C.POINTER(C.c_void_p),

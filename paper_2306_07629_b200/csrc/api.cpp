@@ -992,13 +992,10 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     S->sp.tp_rank = tp ? tp->rank : 0;
     S->sp.tp_max_rows = tp ? tp->max_rows : 0;
     if (tp) {
-        S->sp.tp_recv = static_cast<float*>(tp->buf);
+        S->sp.tp_recv = static_cast<unsigned long long*>(tp->buf);
         S->sp.tp_flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(tp->buf) + tp->recv_bytes);
-        for (uint32_t k = 0; k < tp->world; ++k) {
-            S->sp.tp_peer_recv[k] = static_cast<float*>(tp->peer_base[k]);
-            S->sp.tp_peer_flags[k] = reinterpret_cast<uint32_t*>(
-                static_cast<uint8_t*>(tp->peer_base[k]) + tp->recv_bytes);
-        }
+        for (uint32_t k = 0; k < tp->world; ++k)
+            S->sp.tp_peer_recv[k] = static_cast<unsigned long long*>(tp->peer_base[k]);
     }
     S->sp.trace = nullptr;
     S->sp.dbg = 0;
@@ -1043,8 +1040,8 @@ int dsq_cuda_tp_create(int device, uint32_t world, uint32_t rank, uint32_t max_r
     t->rank = rank;
     t->max_rows = (max_rows + 3) & ~3u;
     t->max_grid = max_grid;
-    t->recv_bytes = size_t(2) * world * t->max_rows * 4;
-    const size_t bytes = t->recv_bytes + size_t(max_grid) * 4;
+    t->recv_bytes = size_t(2) * world * t->max_rows * 8;  // {value, tag} words
+    const size_t bytes = t->recv_bytes + 16;                // + watchdog flag
     cudaError_t e = cudaMalloc(&t->buf, bytes);
     if (e == cudaSuccess) e = cudaMemset(t->buf, 0, bytes);
     if (e == cudaSuccess && ipc_handle) {
@@ -1085,6 +1082,15 @@ int dsq_cuda_tp_connect_local(dsq_cuda_tp* const* ctxs, uint32_t world) {
         for (uint32_t k = 0; k < world; ++k) ctxs[r]->peer_base[k] = ctxs[k]->buf;
     }
     return DSQ_OK;
+}
+
+int dsq_cuda_tp_error(const dsq_cuda_tp* t) {
+    if (!t) return fail(DSQ_E_INVALID_ARGUMENT, "null tp");
+    cudaSetDevice(t->device);
+    uint32_t v = 0;
+    CUDA_TRY(cudaMemcpy(&v, static_cast<const uint8_t*>(t->buf) + t->recv_bytes, 4,
+                        cudaMemcpyDeviceToHost));
+    return v ? fail(DSQ_E_INTERNAL, "tp: a peer never arrived (watchdog fired)") : DSQ_OK;
 }
 
 int dsq_cuda_tp_destroy(dsq_cuda_tp* t) {

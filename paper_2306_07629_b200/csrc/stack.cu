@@ -340,11 +340,17 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j)
                 s += S[j * 128 + min(e - 1 - j * 128, 127u)];
             if (tp) {
-                // a partial sum: hand it to every rank (own included) at
-                // slot [parity][this rank][row]
+                // a partial sum: hand it to every rank (own included) at slot
+                // [parity][this rank][row] as one 64-bit word {value, tag} --
+                // single-copy atomic, so no fence or separate flag is needed
+                // (the receiver polls the tag, NCCL's LL protocol idea)
+                const unsigned long long word =
+                    (static_cast<unsigned long long>(p.tp_base + d.reduce_ord + 1) << 32) |
+                    __float_as_uint(s);
                 for (uint32_t k = 0; k < p.tp_world; ++k)
-                    p.tp_peer_recv[k][(size_t(par) * p.tp_world + p.tp_rank) * p.tp_max_rows +
-                                      r0 + i] = s;
+                    st_volatile_u64(p.tp_peer_recv[k] +
+                                        (size_t(par) * p.tp_world + p.tp_rank) * p.tp_max_rows + r0 + i,
+                                    word);
             } else if (d.y_f16) {
                 static_cast<__half*>(d.y)[r0 + i] = __float2half_rn(s);
             } else {
@@ -352,20 +358,30 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
         }
         if (tp) {
-            // signal the same CTA index on every rank, wait for all ranks'
-            // partials of these rows, then sum them in rank order
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence_system();
-                for (uint32_t k = 0; k < p.tp_world; ++k)
-                    red_release_sys_add(p.tp_peer_flags[k] + cta, 1u);
-            }
-            const uint32_t target = (p.tp_base + d.reduce_ord + 1) * p.tp_world * kFin;
-            while (ld_acquire_sys(p.tp_flags + cta) < target) __nanosleep(32);
-            const float* recv = p.tp_recv + size_t(par) * p.tp_world * p.tp_max_rows;
+            // wait for every rank's tagged partial of these rows and sum them
+            // in rank order (identical on every rank).  Watchdog: a peer that
+            // never arrives (ranks that ran different launch sequences, a dead
+            // peer) must not hang the GPU -- give up after ~4 s and raise the
+            // context's error flag.
+            const uint32_t tag = p.tp_base + d.reduce_ord + 1;
+            const unsigned long long* recv =
+                p.tp_recv + size_t(par) * p.tp_world * p.tp_max_rows;
+            const unsigned long long t_start = gtimer_ns();
             for (uint32_t i = 32 * f + lane; i < nrows; i += 32 * kFin) {
                 float s = 0.f;
-                for (uint32_t k = 0; k < p.tp_world; ++k) s += recv[k * p.tp_max_rows + r0 + i];
+                for (uint32_t k = 0; k < p.tp_world; ++k) {
+                    const unsigned long long* src = recv + k * p.tp_max_rows + r0 + i;
+                    unsigned long long v = ld_volatile_u64(src);
+                    while (uint32_t(v >> 32) != tag) {
+                        if (gtimer_ns() - t_start > 4000000000ull) {
+                            atomicExch(p.tp_flags, 1u);
+                            break;
+                        }
+                        __nanosleep(20);
+                        v = ld_volatile_u64(src);
+                    }
+                    s += __uint_as_float(uint32_t(v));
+                }
                 if (d.y_f16)
                     static_cast<__half*>(d.y)[r0 + i] = __float2half_rn(s);
                 else

@@ -98,14 +98,13 @@ struct StackParams {
     uint32_t smem_bytes;
     // tensor parallelism (world > 1): the partial y of a reduce layer is
     // summed over the ranks' CTAs with the same index over peer memory.
-    // recv = [2 parities][world][max_rows] fp32 per rank, flags = [grid] u32
-    // monotonic arrival counts per rank; peer_* are the (P2P-mapped) buffers
-    // of every rank, own rank included.
+    // recv = [2 parities][world][max_rows] {fp32 value, u32 tag} words per
+    // rank; peer_recv are the (P2P-mapped) buffers of every rank, own rank
+    // included; tp_flags[0] = watchdog error flag of this rank.
     uint32_t tp_world, tp_rank, tp_base, tp_max_rows;
-    float* tp_recv;
+    unsigned long long* tp_recv;
     uint32_t* tp_flags;
-    float* tp_peer_recv[8];
-    uint32_t* tp_peer_flags[8];
+    unsigned long long* tp_peer_recv[8];
     // dev-only experiment switches (DSQ_STACK_DBG): bit 0 skips the decode math
     // (results are garbage; measures the streaming skeleton alone), bit 2
     // records the consumer cycle profile into `trace`

@@ -236,6 +236,10 @@ class TPContext:
         blob = b"".join(handles)
         check(lib.dsq_cuda_tp_connect(self.handle, blob))
 
+    def check(self) -> None:
+        """Raise if a fused reduce's watchdog fired (a peer never arrived)."""
+        check(lib.dsq_cuda_tp_error(self.handle))
+
     @staticmethod
     def connect_local(ctxs: list) -> None:
         arr = (C.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])

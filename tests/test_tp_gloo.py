@@ -116,3 +116,28 @@ def test_tp_shards_on_device(oracle):
             sq, c0, c1 = shard_cols(q, r, world)
             yc += fused_dns_matvec(sq, x[c0:c1])
         assert np.abs(yc - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+def test_decoder_shards_chain_locally():
+    """The row split of every column-parallel producer equals the column split
+    of its row-parallel consumer (o <- v, down <- up), so the fused-reduce
+    stack needs no exchange before a row-parallel layer."""
+    from paper_2306_07629_b200.tp import DECODER, decoder_chain, shard_decoder
+    shp = {"v": (256, 256), "q": (256, 256), "k": (256, 256), "o": (256, 256),
+           "up": (704, 256), "gate": (704, 256), "down": (256, 704)}
+    qls = [to_quantized_layer(make_layer(*shp[n], 3, 0.01, seed=i), name=n)
+           for i, n in enumerate(DECODER)]
+    for world in (2, 4, 8):
+        rows_v, rows_up, cols_o, cols_down = 0, 0, 0, 0
+        for r in range(world):
+            s = shard_decoder(qls, r, world)
+            assert s[3].cols == s[0].rows and s[6].cols == s[4].rows
+            rows_v += s[0].rows
+            rows_up += s[4].rows
+            cols_o += s[3].cols
+            cols_down += s[6].cols
+            assert s[3].rows == 256 and s[6].rows == 256  # row-parallel: full outputs
+        assert rows_v == cols_o == 256 and rows_up == cols_down == 704
+    deps, reduce, _ = decoder_chain(2, 1)
+    assert deps[:7] == [-1, -1, -1, 0, 3, 3, 4] and deps[7:10] == [6, 6, 6]
+    assert [i for i, r in enumerate(reduce) if r] == [3, 6, 10, 13]
