@@ -6,7 +6,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas 
 PKG       := paper_2306_07629_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libdsq_cuda.so
-OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/api.o $(CSRC)/container.o
+OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o
 
 all: $(LIB) oracle cxx-test
 
@@ -16,6 +16,9 @@ $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/layout.hpp $(CSRC)/ptx.cuh
 $(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/stack.ptxas.log || (cat $(CSRC)/stack.ptxas.log; false)
 
+$(CSRC)/batch.o: $(CSRC)/batch.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/batch.ptxas.log || (cat $(CSRC)/batch.ptxas.log; false)
+
 $(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/layout.hpp $(CSRC)/stack.hpp include/dsq_cuda.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC,-fopenmp -c $< -o $@
 
@@ -24,6 +27,15 @@ $(CSRC)/container.o: $(CSRC)/container.cpp include/dsq_cuda.h
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp
+
+# dev: the stack kernel with the per-warp cycle profiler compiled in
+# (tools/stack_prof.py; DSQ_CUDA_LIB=paper_2306_07629_b200/libdsq_cuda_prof.so)
+PROFLIB := $(PKG)/libdsq_cuda_prof.so
+profile-lib: $(PROFLIB)
+$(CSRC)/stack_prof.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
+	$(NVCC) $(NVFLAGS) -DDSQ_STACK_PROFILE -c $< -o $@ 2> /dev/null
+$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 oracle:
 	$(MAKE) -C oracle
@@ -47,4 +59,4 @@ clean:
 	rm -f $(OBJS) $(LIB) $(CSRC)/*.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean cxx-test
+.PHONY: all oracle clean cxx-test profile-lib

@@ -31,6 +31,12 @@ cudaError_t launch_decode(int mode, const LayerParams& P, void* out, cudaStream_
 cudaError_t launch_f32_to_f16(const float* in, uint16_t* out, uint32_t n, cudaStream_t st,
                               bool pdl);
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl);
+cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut,
+                         const uint32_t* row_ptr, const uint32_t* csr, uint32_t rows,
+                         uint32_t cols, uint32_t ns, uint32_t tiles4, const uint16_t* x,
+                         uint32_t x_stride, uint32_t B, void* y, uint32_t y_stride, bool y_f16,
+                         float* part, uint32_t kslices, uint32_t spans_per_slice, int mode,
+                         cudaStream_t st);
 cudaError_t launch_decode_tiles(int mode, uint32_t bits, const uint32_t* idx, const uint32_t* lut,
                                 uint32_t rows, uint32_t cols, uint32_t ns, void* out,
                                 cudaStream_t st);
@@ -300,7 +306,9 @@ struct dsq_cuda_layer {
     uint32_t* stack_counters = nullptr;     // [2]
     float* gseg1 = nullptr;
     cudaStream_t stream = nullptr;
-    std::mutex mu;       // guards dense_w materialization
+    float* batch_part = nullptr;            // batched-product slice partials (lazy)
+    uint32_t batch_kslices = 0, batch_spans = 0;
+    std::mutex mu;       // guards dense_w materialization and batch_part
     std::mutex host_mu;  // serializes the host-buffer API on the internal stream
 };
 
@@ -693,6 +701,7 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     cudaSetDevice(L->device);
     if (L->stream) cudaStreamDestroy(L->stream);
     if (L->dense_w) cudaFree(L->dense_w);
+    if (L->batch_part) cudaFree(L->batch_part);
     if (L->arena) cudaFree(L->arena);
     delete L;
     return DSQ_OK;
@@ -726,11 +735,45 @@ static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
     return DSQ_OK;
 }
 
+// batched products (K8, batch.cu): x [batch][cols] fp16, y [batch][rows]
+static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype, void* y,
+                      int y_dtype, uint32_t batch, cudaStream_t st) {
+    if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_FUSED)
+        return fail(DSQ_E_UNSUPPORTED, "batched products: LUT, CSR or FUSED kernels");
+    if (!L->rec_layout)
+        return fail(DSQ_E_UNSUPPORTED, "batched products need bits 3 or 4 (got %u)", L->bits);
+    if (x_dtype != DSQ_F16) return fail(DSQ_E_INVALID_ARGUMENT, "batched x must be F16");
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) || (L->cols % 8))
+        return fail(DSQ_E_INVALID_ARGUMENT, "batched x rows must be 16-byte aligned (cols %% 8 == 0)");
+    if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
+        return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
+    {
+        std::lock_guard<std::mutex> lk(L->mu);
+        if (!L->batch_part) {
+            // column slices so that (row groups of 128) x slices >= 4 CTAs per SM
+            // (latency hiding for the index-word loads), at most 2 spans each
+            const uint32_t tiles16 = (L->tiles + 3) / 4, groups = (tiles16 + 7) / 8;
+            const uint32_t want = std::max<uint32_t>(1, ceil_div(4u * uint32_t(L->num_sms), groups));
+            L->batch_spans = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(L->ns, want), 2));
+            L->batch_kslices = ceil_div(L->ns, L->batch_spans);
+            CUDA_TRY(cudaMalloc(&L->batch_part,
+                                size_t(L->batch_kslices) * tiles16 * 16 * 16 * sizeof(float)));
+        }
+    }
+    const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
+    CUDA_TRY(launch_batch(L->bits, L->rec, L->tlut, L->P.row_ptr, L->P.csr, L->rows, L->cols,
+                          L->ns, L->tiles, static_cast<const uint16_t*>(x), L->cols, batch, y,
+                          L->rows, y_dtype == DSQ_F16, L->batch_part, L->batch_kslices,
+                          L->batch_spans, mode, st));
+    return DSQ_OK;
+}
+
 static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_dtype, void* y,
                      int y_dtype, uint32_t batch, cudaStream_t st, bool pdl) {
     auto* L = const_cast<dsq_cuda_layer*>(Lc);
     if (!L || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
-    if (batch != 1) return fail(DSQ_E_UNSUPPORTED, "batch must be 1 (ABI v1)");
+    if (batch < 1 || batch > 16) return fail(DSQ_E_INVALID_ARGUMENT, "batch must be 1..16");
+    if (batch > 1) return gemv_batch(L, kernel, x, x_dtype, y, y_dtype, batch, st);
     if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)
         return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);
     if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)

@@ -604,8 +604,25 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         xa = *reinterpret_cast<const uint4*>(xsp);
                         xb2 = *reinterpret_cast<const uint4*>(xsp + 128);
                     };
-                    load(sp, xs);
-                    for (uint32_t k = s; k < s_end; ++k) {
+                    uint32_t k = s;
+                    if constexpr (BITS == 3) {
+                        // span pairs: two independent units per iteration
+                        for (; k + 1 < s_end; k += 2) {
+                            const uint32_t a0 = sp[lane], a1 = sp[32 + lane], a2 = sp[64 + lane];
+                            const uint32_t b0 = sp[96 + lane], b1 = sp[128 + lane],
+                                           b2 = sp[160 + lane];
+                            const uint4 xa0 = *reinterpret_cast<const uint4*>(xs);
+                            const uint4 xb0 = *reinterpret_cast<const uint4*>(xs + 128);
+                            const uint4 xa1 = *reinterpret_cast<const uint4*>(xs + kSpanCols);
+                            const uint4 xb1 = *reinterpret_cast<const uint4*>(xs + kSpanCols + 128);
+                            span3_mma_one(a0, a1, a2, P.a, xa0, xb0, d0);
+                            span3_mma_one(b0, b1, b2, P.a, xa1, xb1, d1);
+                            sp += 2 * UW;
+                            xs += 2 * kSpanCols;
+                        }
+                    }
+                    if (k < s_end) load(sp, xs);
+                    for (; k < s_end; ++k) {
                         uint32_t wc[BITS];
 #pragma unroll
                         for (int q = 0; q < BITS; ++q) wc[q] = w[q];

@@ -111,6 +111,26 @@ __device__ __forceinline__ void span3_mma(uint32_t w0, uint32_t w1, uint32_t w2,
     }
 }
 
+// the same for one unit into a single accumulator set; two independent units
+// interleaved (span pairs) give the scheduler twice the independent work
+__device__ __forceinline__ void span3_mma_one(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const Planes8& P, const uint4& xa, const uint4& xb,
+                                              float (&d)[4]) {
+    const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
+    const uint32_t t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) |
+                       ((w2 >> 1) & 0x44444444u);
+    const uint32_t sA[4] = {m0, hi16(m0), m1, hi16(m1)};
+    const uint32_t sB[4] = {m2, hi16(m2), t, hi16(t)};
+    const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint32_t a0, a1, a2, a3;
+        quad8(sA[j], P, a0, a2);
+        quad8(sB[j], P, a1, a3);
+        hmma16816(d, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+    }
+}
+
 // 4-bit: words w[0..3] (nibble n of w[k] = index 8k+n)
 __device__ __forceinline__ void span4_mma(const uint4& w, const Planes16& P, const uint4& xa,
                                           const uint4& xb, float (&d0)[4], float (&d1)[4]) {
