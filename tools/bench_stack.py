@@ -12,7 +12,13 @@ packed layout (uniformly random 3-bit indices are uniformly random payload
 bytes; CSR positions are cleared to index 0 as quantize_layer does,
 pipeline.cpp:25-32) so 65B shapes build in seconds.
 
+Under torchrun (WORLD_SIZE > 1, one process per GPU) the model runs
+tensor-parallel (configs[3]): v,q,k,up,gate column-parallel, o,down
+row-parallel, the two all-reduces per decoder layer fused into the stack
+kernel over NVLink peer memory; timing is the max over ranks.
+
 usage: python tools/bench_stack.py [--model 13b] [--tokens 3] [--rotation 8]
+       torchrun --nproc-per-node 8 tools/bench_stack.py --model 65b
 """
 import argparse
 import json
@@ -62,10 +68,12 @@ def fast_layer(rows, cols, bits=3, sparsity=0.0045, seed=0):
     return QuantizedLayer(f"{rows}x{cols}", rows, cols, packed, sparse, 10), int(pos.size)
 
 
-def run(model, tokens, rotation, peak):
+def run(model, tokens, rotation, peak, rank=0, world=1):
     import torch
     import paper_2306_07629_b200._native as N
     from paper_2306_07629_b200 import DeviceLayer, DeviceStack
+    from paper_2306_07629_b200.dsq import TPContext
+    from paper_2306_07629_b200.tp import decoder_chain, shard_decoder
     from oracle.oracle import make_x
     h, f, nl = MODELS[model]
     shp = shapes(h, f)
@@ -79,49 +87,61 @@ def run(model, tokens, rotation, peak):
         nnzs.append(nz)
     bytes_dec = sum(int(N.lib.dsq_bytes_touched_estimate(r, c, 3, 0, nz))
                     for (_, r, c), nz in zip(shp, nnzs))
-    dls = [[DeviceLayer(q) for q in qls] for _ in range(rotation)]
+    shards = shard_decoder(qls, rank, world) if world > 1 else qls
+    dev = torch.cuda.current_device()
+    dls = [[DeviceLayer(q, device=dev) for q in shards] for _ in range(rotation)]
     x = torch.from_numpy(make_x(h).view(np.int16)).cuda()
-    ys = [[torch.empty(r, dtype=torch.int16, device="cuda") for (_, r, _) in shp]
+    ys = [[torch.empty(q.rows, dtype=torch.int16, device="cuda") for q in shards]
           for _ in range(rotation)]
+    tp = None
+    if world > 1:
+        import torch.distributed as dist
+        tp = TPContext(world, rank, max_rows=h,
+                       max_grid=torch.cuda.get_device_properties(dev).multi_processor_count,
+                       device=dev)
+        handles = [None] * world
+        dist.all_gather_object(handles, tp.ipc_handle)
+        tp.connect(handles)
     setup = time.time() - t0
 
     def build(ntok):
-        layers, deps, xp, yp = [], [], [], []
-        prev = -1
+        deps, reduce, _ = decoder_chain(ntok * nl, 1)
+        layers, yp = [], []
         for t in range(ntok * nl):
             slot = t % rotation
-            base = len(layers)
-            for j, dl in enumerate(dls[slot]):
-                layers.append(dl)
-                if CHAIN_IN[j] < 0 and prev < 0:
-                    deps.append(-1)
-                    xp.append(x.data_ptr())
-                else:
-                    deps.append(prev if CHAIN_IN[j] < 0 else base + CHAIN_IN[j])
-                    xp.append(0)
-                yp.append(ys[slot][j].data_ptr())
-            prev = base + 6
-        return DeviceStack(layers, deps, xp, yp, N.F16)
+            layers += dls[slot]
+            yp += [y.data_ptr() for y in ys[slot]]
+        xp = [x.data_ptr() if d < 0 else 0 for d in deps]
+        if tp is None:
+            return DeviceStack(layers, deps, xp, yp, N.F16)
+        return DeviceStack(layers, deps, xp, yp, N.F16, reduce=reduce, tp=tp)
 
     warm, timed = build(1), build(tokens)
     warm.run(0)
     timed.run(0)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     timed.run(0)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if world > 1:
+        tp.check()
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     gemvs = tokens * nl * 7
     gbs = bytes_dec * nl * tokens / (ms * 1e-3) / 1e9
     return {
         "model": f"llama-{model} linear stack ({nl} decoder layers x 7 GEMVs, 3-bit + 0.45% CSR)",
-        "tokens": tokens, "gpus": 1, "parallelism": "tp1",
+        "tokens": tokens, "gpus": world, "parallelism": f"tp{world}",
         "us_per_gemv": round(ms * 1e3 / gemvs, 3),
         "ms_per_token": round(ms / tokens, 4),
         "decode_tok_s_linear": round(tokens / (ms * 1e-3), 1),
-        "effective_GBs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
+        "effective_GBs": round(gbs, 1), "frac_of_peak_per_gpu": round(gbs / world / peak, 4),
         "bytes_per_token": bytes_dec * nl, "rotation": rotation, "setup_s": round(setup, 1),
     }
 
@@ -136,8 +156,20 @@ def main():
         peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except Exception:
         peak = 6650.0
+    import os
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     for m in (list(MODELS) if args.model == "all" else [args.model]):
-        print(json.dumps(run(m, args.tokens, args.rotation, peak)), flush=True)
+        line = run(m, args.tokens, args.rotation, peak, rank, world)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
