@@ -13,7 +13,7 @@ all: $(LIB) oracle cxx-test
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/layout.hpp $(CSRC)/ptx.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/kernels.ptxas.log || (cat $(CSRC)/kernels.ptxas.log; false)
 
-$(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layout.hpp
+$(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layout.hpp $(CSRC)/tile.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/stack.ptxas.log || (cat $(CSRC)/stack.ptxas.log; false)
 
 $(CSRC)/batch.o: $(CSRC)/batch.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh
@@ -35,6 +35,14 @@ profile-lib: $(PROFLIB)
 $(CSRC)/stack_prof.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_PROFILE -c $< -o $@ 2> /dev/null
 $(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
+
+# debug variant: bounded waits that trap with the waiting site (stack.cu)
+WDLIB := $(PKG)/libdsq_cuda_wd.so
+watchdog-lib: $(WDLIB)
+$(CSRC)/stack_wd.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
+	$(NVCC) $(NVFLAGS) -DDSQ_STACK_WATCHDOG -c $< -o $@
+$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 oracle:
@@ -59,4 +67,4 @@ clean:
 	rm -f $(OBJS) $(LIB) $(CSRC)/*.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean cxx-test profile-lib
+.PHONY: all oracle clean cxx-test profile-lib watchdog-lib

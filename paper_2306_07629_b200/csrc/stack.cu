@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdint>
 
 #include "layout.hpp"
@@ -90,6 +91,40 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+
+#ifdef DSQ_STACK_WATCHDOG
+// debug build (make watchdog-lib): every mbarrier wait and dependency poll of
+// the stack kernel gives up after ~2 s with the waiting site printed, so a
+// protocol deadlock turns into a trap with a location instead of a hung GPU
+__device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int line) {
+    const unsigned long long t0 = gtimer_ns();
+    while (!mbar_try_wait(bar, parity)) {
+        if (gtimer_ns() - t0 > 2000000000ull) {
+            if ((threadIdx.x & 31) == 0)
+                printf("stack watchdog: cta %u warp %u line %d parity %u\n", blockIdx.x,
+                       threadIdx.x >> 5, line, parity);
+            __trap();
+        }
+    }
+}
+#define mbar_wait(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
+#define DSQ_WD_POLL(cond, ...)                                \
+    do {                                                      \
+        const unsigned long long wd0_ = gtimer_ns();          \
+        while (cond) {                                        \
+            if (gtimer_ns() - wd0_ > 2000000000ull) {         \
+                printf(__VA_ARGS__);                          \
+                __trap();                                     \
+            }                                                 \
+            __nanosleep(20);                                  \
+        }                                                     \
+    } while (0)
+#else
+#define DSQ_WD_POLL(cond, ...)          \
+    do {                                \
+        while (cond) __nanosleep(20);   \
+    } while (0)
+#endif
 #define DSQ_TRACE(l, slot)                                                                 \
     do {                                                                                   \
         if (p.trace && !(p.dbg & 4u))                                                      \
@@ -292,7 +327,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
             if (d.dep != kNoDep) {
                 if (lane == 0) {
-                    while (ld_acquire_gpu(p.counters + d.dep) < G * (1 + kCsrWarps)) __nanosleep(20);
+                    DSQ_WD_POLL(ld_acquire_gpu(p.counters + d.dep) < G * (1 + kCsrWarps),
+                                "stack watchdog: cta %u layer %u dep %u counter %u\n", cta, l, d.dep,
+                                *(volatile const uint32_t*)(p.counters + d.dep));
                     DSQ_TRACE(l, kTrDepMet);
                 }
                 __syncwarp();
