@@ -403,6 +403,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         except Exception:
             traffic = None
     per_rank = value / world
+    # the roofline model's prediction (paper_2306_07629_b200/roofline.py):
+    # reference-charged bytes of the step's 7 GEMVs at the HBM peak
+    from paper_2306_07629_b200 import roofline as RL
+    hw = RL.b200_profile()
+    pred_us = sum(RL.gemv_cost(r, c, 3, L.nnz, hw).predicted_time
+                  for L, (_, r, c) in zip(host_layers, SHAPES)) * 1e6
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -416,7 +422,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "unit": "GB/s", "frac": round(per_rank / peak, 4), "traffic": traffic,
                      "kernel": kernel_name,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback",
-                     "algorithmic_bytes_per_step": bytes_step},
+                     "algorithmic_bytes_per_step": bytes_step,
+                     "model": {"profile": hw.name, "predicted_us_per_step": round(pred_us, 3),
+                               "measured_us_per_step": round(ms_step * 1e3, 3)}},
         "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
         "gemvs_timed": args.steps * len(SHAPES), "mode": args.mode,
         "schedule": {"workers": info.workers, "ctas": info.ctas},

@@ -270,6 +270,63 @@ dsq_cuda_layer* dsq_cuda_container_layer(const dsq_cuda_container* c, uint32_t i
 const char* dsq_cuda_container_layer_name(const dsq_cuda_container* c, uint32_t index);
 int dsq_cuda_container_close(dsq_cuda_container* c);
 
+/* ---- roofline model (reference include/dsq/roofline.hpp:10-88) ----------- */
+/* The reference's analytical decode-step model (src/roofline.cpp:10-209,
+ * `dsq profile` tools/dsq.cpp:220-271) with the same formulas and errors
+ * (invalid_argument for bad shapes / profiles, missing_file and
+ * malformed_header from the JSON loaders), a B200 HardwareProfile, and the
+ * cost of one fused Dense-and-Sparse LUT-GEMV of the path. */
+typedef struct dsq_hw_profile {
+    char name[64];
+    double peak_flops;     /* operations per second */
+    double mem_bandwidth;  /* bytes per second      */
+} dsq_hw_profile;
+
+typedef struct dsq_model_shape {
+    char name[64];
+    uint32_t num_layers, hidden_dim, ffn_dim, num_heads, vocab_size;
+    uint32_t seq_len;          /* reference default 128 */
+    uint32_t weight_bits;      /* 2..16                 */
+    uint32_t activation_bits;  /* fixed 16              */
+} dsq_model_shape;
+
+enum { DSQ_LAYER_FC = 0, DSQ_LAYER_ATTENTION = 1, DSQ_LAYER_OTHER = 2 };
+/* entries of dsq_decode_step_costs: qkv_proj, out_proj, ffn_gate, ffn_up,
+ * ffn_down, lm_head, attn_kv, other */
+#define DSQ_DECODE_COSTS 8
+
+typedef struct dsq_layer_cost {
+    char name[32];
+    int kind;               /* DSQ_LAYER_* */
+    double flops, weight_elems, activation_elems, weight_bytes, activation_bytes;
+    double predicted_s;     /* max(flops / peak_flops, bytes / mem_bandwidth) */
+    int memory_bound;       /* bytes / bw >= flops / peak                     */
+    double intensity;       /* flops per memory element (0 if undefined)      */
+} dsq_layer_cost;
+
+/* costs[DSQ_DECODE_COSTS]; total / weight_traffic_share may be NULL */
+int dsq_decode_step_costs(const dsq_model_shape* shape, const dsq_hw_profile* hw,
+                          dsq_layer_cost* costs, dsq_layer_cost* total,
+                          double* weight_traffic_share);
+int dsq_arithmetic_intensity(const dsq_layer_cost* cost, double* out);
+/* predicted decode-step seconds per weight bit width, and normalised to 16-bit */
+int dsq_predicted_runtime_curve(const dsq_model_shape* shape, const dsq_hw_profile* hw,
+                                const uint32_t* bits, uint32_t n, double* seconds,
+                                double* normalized);
+int dsq_affine_fit_r2(const uint32_t* bits, const double* normalized, uint32_t n, double* r2);
+/* JSON files: {"name", "peak_flops", "mem_bandwidth_bytes_per_s"} and
+ * {"name", "num_layers", "hidden_dim", "ffn_dim", "num_heads", "vocab_size",
+ *  ["seq_len"], ["weight_bits"]} (roofline.cpp:171-209) */
+int dsq_load_hardware_profile(const char* path, dsq_hw_profile* out);
+int dsq_load_model_shape(const char* path, dsq_model_shape* out);
+/* B200 from MEASURED_PEAKS.json ("hbm_gbs", "bf16_tflops"; NULL or absent:
+ * the fallback 6.65 TB/s, 1.59 PFLOP/s) */
+int dsq_hw_profile_b200(const char* measured_peaks_json, dsq_hw_profile* out);
+/* one fused LUT-GEMV (rows x cols, bits, nnz outliers, batch): charged bytes
+ * of kernels.cpp:205-212 (x / y per batch row), 2*B*(rows*cols+nnz) flops */
+int dsq_gemv_cost(uint32_t rows, uint32_t cols, uint32_t bits, uint64_t nnz, uint32_t batch,
+                  const dsq_hw_profile* hw, dsq_layer_cost* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,24 @@ class ContainerMeta(C.Structure):
     ]
 
 
+class HwProfile(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("peak_flops", C.c_double), ("mem_bandwidth", C.c_double)]
+
+
+class ModelShape(C.Structure):
+    _fields_ = [("name", C.c_char * 64)] + [(k, C.c_uint32) for k in (
+        "num_layers", "hidden_dim", "ffn_dim", "num_heads", "vocab_size", "seq_len",
+        "weight_bits", "activation_bits")]
+
+
+class LayerCost(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("kind", C.c_int)] + [(k, C.c_double) for k in (
+        "flops", "weight_elems", "activation_elems", "weight_bytes", "activation_bytes",
+        "predicted_s")] + [("memory_bound", C.c_int), ("intensity", C.c_double)]
+
+
+DECODE_COSTS = 8
+
 # every symbol declared in include/dsq_cuda.h, with its ctypes prototype
 PROTOTYPES = {
     "dsq_cuda_abi_version": (C.c_int, []),
@@ -133,6 +151,20 @@ PROTOTYPES = {
     "dsq_cuda_container_layer": (C.c_void_p, [C.c_void_p, C.c_uint32]),
     "dsq_cuda_container_layer_name": (C.c_char_p, [C.c_void_p, C.c_uint32]),
     "dsq_cuda_container_close": (C.c_int, [C.c_void_p]),
+    "dsq_decode_step_costs": (C.c_int, [C.POINTER(ModelShape), C.POINTER(HwProfile),
+                                        C.POINTER(LayerCost), C.POINTER(LayerCost),
+                                        C.POINTER(C.c_double)]),
+    "dsq_arithmetic_intensity": (C.c_int, [C.POINTER(LayerCost), C.POINTER(C.c_double)]),
+    "dsq_predicted_runtime_curve": (C.c_int, [C.POINTER(ModelShape), C.POINTER(HwProfile),
+                                              C.POINTER(C.c_uint32), C.c_uint32,
+                                              C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "dsq_affine_fit_r2": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.c_uint32,
+                                    C.POINTER(C.c_double)]),
+    "dsq_load_hardware_profile": (C.c_int, [C.c_char_p, C.POINTER(HwProfile)]),
+    "dsq_load_model_shape": (C.c_int, [C.c_char_p, C.POINTER(ModelShape)]),
+    "dsq_hw_profile_b200": (C.c_int, [C.c_char_p, C.POINTER(HwProfile)]),
+    "dsq_gemv_cost": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                                C.POINTER(HwProfile), C.POINTER(LayerCost)]),
 }
 
 
