@@ -529,7 +529,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
             if (pa < pe) {
                 const uint32_t n = min(pcu, pe - pa);
-                if (lane == 0) {
+                if (lane == 0 && !(p.dbg & 8u)) {
                     uint64_t* bar = &full[cw * WS + pslot];
                     mbar_arrive_expect_tx(bar, n * UW * 4);
                     bulk_g2s(ring + size_t(cw * WS + pslot) * p.slot_bytes, psrc, n * UW * 4, bar,
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         };
         for (uint32_t cb = u0; cb < u1; cb += cu) {
             DSQ_LAP(c_dense);
-            mbar_wait(&full[cw * WS + cslot], cphase);
+            if (!(p.dbg & 8u)) mbar_wait(&full[cw * WS + cslot], cphase);  // dbg 8: compute only
             DSQ_LAP(c_fw);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(cw * WS + cslot) * p.slot_bytes);
             uint32_t u = cb;

@@ -133,6 +133,19 @@ __global__ void __launch_bounds__(768) k_hmma(int niter, float* out, Clk* clk, u
       } else if (VAR == 5) {   // the product's span3_mma (dual accumulators)
         sqz::Planes8 PP{P[r].l0, P[r].l1, P[r].h0, P[r].h1};
         sqz::span3_mma(wp[0], wp[32], wp[64], PP, xa, xb, d[r], d2[r]);
+      } else if (VAR == 7 || VAR == 8) {   // the stack kernel's span-pair loop: 2 units / iter
+        sqz::Planes8 PP{P[r].l0, P[r].l1, P[r].h0, P[r].h1};
+        const int s2 = (s + 1) & (NSPAN - 1);
+        const uint32_t* wq = pk + (s2 * RT + r) * WPS * 32 + lane;
+        const uint4* xq = reinterpret_cast<const uint4*>(sx + s2 * 128);
+        const uint4 xa2 = xq[xo], xb2 = xq[xo + (XCF ? 16 : 1)];
+        if (VAR == 7) {
+          sqz::span3_mma_one(wp[0], wp[32], wp[64], PP, xa, xb, d[r]);
+          sqz::span3_mma_one(wq[0], wq[32], wq[64], PP, xa2, xb2, d2[r]);
+        } else {
+          sqz::span3_mma(wp[0], wp[32], wp[64], PP, xa, xb, d[r], d2[r]);
+          sqz::span3_mma(wq[0], wq[32], wq[64], PP, xa2, xb2, d[r], d2[r]);
+        }
       } else if (VAR == 6) {   // + IMAD.HI spare-index gather
         sqz::Planes8 PP{P[r].l0, P[r].l1, P[r].h0, P[r].h1};
         sqz::span3_mma<true>(wp[0], wp[32], wp[64], PP, xa, xb, d[r], d2[r], sqz::ShiftK{k29, k30, k31});
@@ -172,7 +185,7 @@ int main(){
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     Clk h; cudaMemcpy(&h, clk, sizeof(Clk), cudaMemcpyDeviceToHost);
     const double ghz = double(h.c1-h.c0)/double(h.t1-h.t0);
-    const double weights = double(grid) * warps * niter * rt * 1024.0;   // 4 rows x 256 cols per span per tile
+    const double weights = double(grid) * warps * niter * rt * 1024.0 * (var >= 7 ? 2 : 1);   // 4 rows x 256 cols per span per tile
     const double wpc = weights / (ms*1e-3) / (ghz*1e9) / nsm;
     const double bpw = var == 2 ? 0.5 : 0.375;
     printf("%-34s warps %2d ctas %d: %.3f ms %.2f GHz  %.1f w/clk/SM  => %.0f GB/s equiv (at 1.965 GHz: %.0f)\n", name, warps, ctas, ms, ghz, wpc,
@@ -184,6 +197,8 @@ int main(){
     run(k_hmma<6,1,1>, "3b product+imad RT1 xcf", 6, 1, warps, 1);
     run(k_hmma<5,2,1>, "3b product RT2 xcf", 5, 2, warps, 1);
     run(k_hmma<6,2,1>, "3b product+imad RT2 xcf", 6, 2, warps, 1);
+    run(k_hmma<7,1,1>, "3b stack span-pair (one acc/unit)", 7, 1, warps, 1);
+    run(k_hmma<8,1,1>, "3b span-pair dual acc", 8, 1, warps, 1);
 
   }
   return 0;
