@@ -327,6 +327,32 @@ int dsq_hw_profile_b200(const char* measured_peaks_json, dsq_hw_profile* out);
 int dsq_gemv_cost(uint32_t rows, uint32_t cols, uint32_t bits, uint64_t nnz, uint32_t batch,
                   const dsq_hw_profile* hw, dsq_layer_cost* out);
 
+/* ---- GPU channel-wise quantization (the step upstream of the path) ------ */
+/* dsq::quantize_channelwise (reference src/nuq.cpp:673-779): one codebook of
+ * 2^bits centroids per output row (group_size 0) or per column group, by
+ * weighted 1-D k-means (weighted_kmeans_1d nuq.cpp:411-502: weighted-quantile
+ * init, Lloyd, exact boundary refinement, merge/split escape), unweighted
+ * k-means or round-to-nearest levels; masked positions (already in the
+ * sparse part) are excluded and get index 0xFFFF.  Bit-identical codebooks,
+ * assignments and objectives to the reference (one CTA per group, exact
+ * sequential-order reductions).  Host arrays in and out. */
+typedef struct dsq_quant_config {  /* dsq::QuantConfig (nuq.hpp:26-37) */
+    uint32_t bits;                 /* 2..8                               */
+    double sensitive_fraction;     /* [0, 0.05]                          */
+    double outlier_fraction;       /* [0, 0.05]                          */
+    uint32_t group_size;           /* 0: channel-wise, else divides cols */
+    uint32_t kmeans_max_iters;     /* >= 1                               */
+    double kmeans_tol;             /* >= 0                               */
+    uint64_t seed;
+} dsq_quant_config;
+enum { DSQ_CODEBOOK_WEIGHTED_KMEANS = 0, DSQ_CODEBOOK_UNWEIGHTED_KMEANS = 1, DSQ_CODEBOOK_RTN = 2 };
+/* w, sens: [rows*cols]; mask: [rows*cols] or NULL; centroids out:
+ * [rows * groups_per_row * 2^bits]; assign out: [rows*cols] */
+int dsq_cuda_quantize_channelwise(const float* w, const float* sens, const uint8_t* mask,
+                                  uint32_t rows, uint32_t cols, const dsq_quant_config* cfg,
+                                  int method, int device, float* centroids, uint16_t* assign,
+                                  double* weighted_objective, double* unweighted_mse_sum);
+
 #ifdef __cplusplus
 }
 #endif

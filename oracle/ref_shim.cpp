@@ -14,6 +14,7 @@
 
 #include "dsq/container.hpp"
 #include "dsq/kernels.hpp"
+#include "dsq/nuq.hpp"
 #include "dsq/packfmt.hpp"
 #include "dsq/pipeline.hpp"
 #include "dsq/sensitivity.hpp"
@@ -267,6 +268,34 @@ int ref_load_container_layer(const char* path, uint32_t index, RefLayer** out) {
         auto* h = new RefLayer;
         h->l = c.layers[index];
         *out = h;
+    });
+}
+
+
+// dsq::quantize_channelwise (nuq.cpp:673-779) on flat arrays: the GPU
+// quantizer's (csrc/quantize.cu) parity reference.  mask may be null.
+int ref_quantize_channelwise(const float* w, const float* sens, const uint8_t* mask,
+                             uint32_t rows, uint32_t cols, uint32_t bits, uint32_t group_size,
+                             uint32_t max_iters, double tol, int method, float* centroids,
+                             uint16_t* assign, double* obj, double* mse) {
+    return guarded([&] {
+        const size_t n = size_t(rows) * cols;
+        WeightMatrix m = make_matrix("matrix", rows, cols, std::vector<float>(w, w + n));
+        QuantConfig cfg;
+        cfg.bits = bits;
+        cfg.group_size = group_size;
+        cfg.kmeans_max_iters = max_iters;
+        cfg.kmeans_tol = tol;
+        std::vector<uint8_t> mk;
+        if (mask) mk.assign(mask, mask + n);
+        const ChannelwiseResult r = quantize_channelwise(
+            m, std::vector<float>(sens, sens + n), cfg, mk, static_cast<CodebookMethod>(method));
+        const uint32_t k = 1u << bits;
+        for (size_t g = 0; g < r.codebooks.size(); ++g)
+            std::memcpy(centroids + g * k, r.codebooks[g].centroids.data(), k * sizeof(float));
+        std::memcpy(assign, r.assignment.data(), n * sizeof(uint16_t));
+        *obj = r.weighted_objective;
+        *mse = r.unweighted_mse_sum;
     });
 }
 

@@ -105,6 +105,12 @@ class LayerCost(C.Structure):
 
 DECODE_COSTS = 8
 
+
+class QuantConfig(C.Structure):
+    _fields_ = [("bits", C.c_uint32), ("sensitive_fraction", C.c_double),
+                ("outlier_fraction", C.c_double), ("group_size", C.c_uint32),
+                ("kmeans_max_iters", C.c_uint32), ("kmeans_tol", C.c_double), ("seed", C.c_uint64)]
+
 # every symbol declared in include/dsq_cuda.h, with its ctypes prototype
 PROTOTYPES = {
     "dsq_cuda_abi_version": (C.c_int, []),
@@ -163,6 +169,10 @@ PROTOTYPES = {
     "dsq_load_hardware_profile": (C.c_int, [C.c_char_p, C.POINTER(HwProfile)]),
     "dsq_load_model_shape": (C.c_int, [C.c_char_p, C.POINTER(ModelShape)]),
     "dsq_hw_profile_b200": (C.c_int, [C.c_char_p, C.POINTER(HwProfile)]),
+    "dsq_cuda_quantize_channelwise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                                C.c_uint32, C.POINTER(QuantConfig), C.c_int,
+                                                C.c_int, C.c_void_p, C.c_void_p,
+                                                C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "dsq_gemv_cost": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
                                 C.POINTER(HwProfile), C.POINTER(LayerCost)]),
 }

@@ -1,0 +1,126 @@
+// C ABI of the GPU channel-wise quantizer (K9, quantize.cu): the reference's
+// dsq::quantize_channelwise (src/nuq.cpp:673-779) with the same validation
+// order and error codes (WeightMatrix::validate tensor.cpp:12-20,
+// QuantConfig::validate nuq.cpp:24-34, group_size / empty_channel checks).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "../../include/dsq_cuda.h"
+#include "quantize.hpp"
+
+extern "C" int dsq_internal_fail(int code, const char* fmt, ...);
+
+namespace {
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 1); }
+};
+}  // namespace
+
+extern "C" int dsq_cuda_quantize_channelwise(const float* w, const float* sens,
+                                             const uint8_t* mask, uint32_t rows, uint32_t cols,
+                                             const dsq_quant_config* cfg, int method, int device,
+                                             float* centroids, uint16_t* assign,
+                                             double* weighted_objective,
+                                             double* unweighted_mse_sum) {
+    if (!cfg || !centroids || !assign)
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "quantize_channelwise: null argument");
+    // matrix.validate()
+    if (rows < 1 || cols < 1)
+        return dsq_internal_fail(DSQ_E_EMPTY_DIMENSION, "matrix: dimensions must be >= 1");
+    if (!w) return dsq_internal_fail(DSQ_E_SHAPE_MISMATCH, "matrix: value count does not match rows*cols");
+    const size_t total = size_t(rows) * cols;
+    for (size_t i = 0; i < total; ++i)
+        if (!std::isfinite(w[i])) return dsq_internal_fail(DSQ_E_NON_FINITE_VALUE, "matrix: non-finite value");
+    // cfg.validate()
+    if (cfg->bits < 2 || cfg->bits > 8)
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "bits must be in 2..8");
+    if (!(cfg->sensitive_fraction >= 0.0 && cfg->sensitive_fraction <= 0.05))
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "sensitive_fraction must be in [0, 0.05]");
+    if (!(cfg->outlier_fraction >= 0.0 && cfg->outlier_fraction <= 0.05))
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "outlier_fraction must be in [0, 0.05]");
+    if (!(cfg->sensitive_fraction + cfg->outlier_fraction < 1.0))
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "fraction sum must be < 1");
+    if (cfg->kmeans_max_iters < 1)
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "kmeans_max_iters must be >= 1");
+    if (!(cfg->kmeans_tol >= 0.0))
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "kmeans_tol must be >= 0");
+    if (!sens) return dsq_internal_fail(DSQ_E_SHAPE_MISMATCH, "matrix: sensitivity shape mismatch");
+    uint32_t gcols = cols;
+    if (cfg->group_size > 0) {
+        if (cols % cfg->group_size != 0)
+            return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "matrix: group_size does not divide cols");
+        gcols = cfg->group_size;
+    }
+    if (method < DSQ_CODEBOOK_WEIGHTED_KMEANS || method > DSQ_CODEBOOK_RTN)
+        return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "quantize_channelwise: unknown method");
+    const uint32_t gpr = cols / gcols, k = 1u << cfg->bits;
+    const size_t groups = size_t(rows) * gpr;
+    size_t np = 1;
+    while (np < gcols) np <<= 1;
+
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return dsq_internal_fail(DSQ_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const uint32_t grid = uint32_t(std::min<size_t>(groups, size_t(sms > 0 ? sms : 1) * 8));
+    const size_t stride = sqz::kmeans_scratch_stride(gcols, np);
+    DevBuf dw, ds, dm, dc, da, dobj, dmse, dfail, dscr;
+    if ((e = dw.alloc(total * 4)) || (e = ds.alloc(total * 4)) ||
+        (e = dm.alloc(mask ? total : 1)) || (e = dc.alloc(groups * k * 4)) ||
+        (e = da.alloc(total * 2)) || (e = dobj.alloc(groups * 8)) || (e = dmse.alloc(groups * 8)) ||
+        (e = dfail.alloc(groups)) || (e = dscr.alloc(stride * grid)))
+        return dsq_internal_fail(DSQ_E_CUDA, "quantize_channelwise: cudaMalloc: %s", cudaGetErrorString(e));
+    if ((e = cudaMemcpy(dw.p, w, total * 4, cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(ds.p, sens, total * 4, cudaMemcpyHostToDevice)) ||
+        (mask && (e = cudaMemcpy(dm.p, mask, total, cudaMemcpyHostToDevice))) ||
+        (e = cudaMemset(dfail.p, 0, groups)))
+        return dsq_internal_fail(DSQ_E_CUDA, "quantize_channelwise: upload: %s", cudaGetErrorString(e));
+    sqz::QuantParams P{};
+    P.w = static_cast<const float*>(dw.p);
+    P.sens = static_cast<const float*>(ds.p);
+    P.mask = mask ? static_cast<const uint8_t*>(dm.p) : nullptr;
+    P.rows = rows;
+    P.cols = cols;
+    P.groups_per_row = gpr;
+    P.bits = cfg->bits;
+    P.max_iters = cfg->kmeans_max_iters;
+    P.tol = cfg->kmeans_tol;
+    P.method = method;
+    P.centroids = static_cast<float*>(dc.p);
+    P.assign = static_cast<uint16_t*>(da.p);
+    P.group_obj = static_cast<double*>(dobj.p);
+    P.group_mse = static_cast<double*>(dmse.p);
+    P.group_failed = static_cast<uint8_t*>(dfail.p);
+    P.scratch = static_cast<uint8_t*>(dscr.p);
+    P.scratch_stride = stride;
+    P.npow2 = np;
+    if ((e = sqz::launch_kmeans(P, grid, 0)) || (e = cudaDeviceSynchronize()))
+        return dsq_internal_fail(DSQ_E_CUDA, "kmeans_groups: %s", cudaGetErrorString(e));
+    std::vector<uint8_t> failed(groups);
+    std::vector<double> obj(groups), mse(groups);
+    if ((e = cudaMemcpy(failed.data(), dfail.p, groups, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(obj.data(), dobj.p, groups * 8, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(mse.data(), dmse.p, groups * 8, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(centroids, dc.p, groups * k * 4, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(assign, da.p, total * 2, cudaMemcpyDeviceToHost)))
+        return dsq_internal_fail(DSQ_E_CUDA, "quantize_channelwise: download: %s", cudaGetErrorString(e));
+    for (size_t g = 0; g < groups; ++g)
+        if (failed[g] == 2) return dsq_internal_fail(DSQ_E_INVALID_ARGUMENT, "kmeans: negative weight");
+    for (size_t g = 0; g < groups; ++g)
+        if (failed[g] == 1)
+            return dsq_internal_fail(DSQ_E_EMPTY_CHANNEL, "matrix: mask covers an entire channel/group");
+    double so = 0.0, sm = 0.0;  // summed in group order (nuq.cpp:774-777)
+    for (size_t g = 0; g < groups; ++g) {
+        so += obj[g];
+        sm += mse[g];
+    }
+    if (weighted_objective) *weighted_objective = so;
+    if (unweighted_mse_sum) *unweighted_mse_sum = sm;
+    return DSQ_OK;
+}
