@@ -16,7 +16,7 @@
 // record moves, the scan resumes after it).  Compiled with -fmad=false so no
 // a*b+c is contracted (the reference's x86-64 build has no FMA).
 //
-// One CTA (128 threads) per group, persistent over groups; per-CTA scratch
+// One CTA (256 threads) per group, persistent over groups; per-CTA scratch
 // in global memory (L1/L2 resident) sized for the group length.
 #include <cuda_runtime.h>
 
@@ -27,7 +27,7 @@
 namespace sqz {
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;
 constexpr uint16_t kMasked = 0xFFFF;
 constexpr uint32_t kMaxK = 256;
 
@@ -189,6 +189,8 @@ __device__ void assign_and_repair(const Scratch& S, Shared& sh, uint32_t k) {
     __syncthreads();
 }
 
+__device__ void intervals(const Scratch& S, Shared& sh, uint32_t k);
+
 // Lloyd until the relative centroid movement is under tol (nuq.cpp:187-225)
 __device__ uint32_t lloyd(const Scratch& S, Shared& sh, uint32_t k, uint32_t max_iters, double tol) {
     const uint32_t n = sh.n, tid = threadIdx.x;
@@ -196,10 +198,13 @@ __device__ uint32_t lloyd(const Scratch& S, Shared& sh, uint32_t k, uint32_t max
     while (iters < max_iters) {
         assign_and_repair(S, sh, k);
         ++iters;
-        // per-cluster sums in position order: thread j owns cluster j
+        // per-cluster sums in position order: thread j owns cluster j and
+        // scans its members' span [first, last]
+        intervals(S, sh, k);
         for (uint32_t j = tid; j < k; j += kThreads) {
             double nu = 0.0, de = 0.0, pl = 0.0;
-            for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t i1 = sh.counts[j] ? sh.ivs[j] + 1 : 0;
+            for (uint32_t i = sh.ivf[j]; i < i1; ++i) {
                 if (S.assign[i] != j) continue;
                 nu += S.w[i] * S.v[i];
                 de += S.w[i];
@@ -253,72 +258,152 @@ __device__ void intervals(const Scratch& S, Shared& sh, uint32_t k) {
     __syncthreads();
 }
 
-// exact boundary re-optimisation (nuq.cpp:246-327); returns true if changed
+// block-wide minimum of cost(m) over m in [m0, m1) (+inf if empty)
+template <class F>
+__device__ double block_min(Shared& sh, uint32_t m0, uint32_t m1, F cost) {
+    const uint32_t tid = threadIdx.x;
+    double v = __longlong_as_double(0x7ff0000000000000ll);
+    for (uint32_t m = m0 + tid; m < m1; m += kThreads) {
+        const double c = cost(m);
+        v = c < v ? c : v;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    __syncthreads();
+    if ((tid & 31) == 0) sh.red_d[tid >> 5] = v;
+    __syncthreads();
+    double r = sh.red_d[0];
+    for (int q = 1; q < kThreads / 32; ++q) r = sh.red_d[q] < r ? sh.red_d[q] : r;
+    return r;
+}
+
+// exact boundary re-optimisation (nuq.cpp:246-327); returns true if changed.
+// Whole block: a scan range (a pairwise cut, or one row m1 of the joint
+// three-cluster cut) is first reduced to its minimum in parallel; only a
+// range whose minimum beats the running record by the margin -- i.e. one
+// where the reference accepts at least one cut -- is replayed exactly by
+// warp 0's chain scan.  Rows m1 are evaluated kThreads/32 at a time (one per
+// warp) and consumed in order, so the break on `left >= best` is the
+// reference's.
 __device__ bool boundary_refine(const Scratch& S, Shared& sh, uint32_t k) {
     if (k < 2) return false;
     intervals(S, sh, k);
     for (uint32_t j = 0; j < k; ++j)
         if (sh.counts[j] == 0) return false;
-    const uint32_t tid = threadIdx.x;
-    if (tid < 32) {
-        bool any = false;
-        for (int sweep = 0; sweep < 32; ++sweep) {
-            bool changed = false;
-            for (uint32_t c = 0; c + 1 < k; ++c) {  // pairwise cuts
-                const uint32_t s = sh.ivf[c], e = sh.ivs[c + 1], cur = sh.ivs[c];
-                const double cc = icost(S, s, cur) + icost(S, cur + 1, e);
-                double best = cc;
-                uint32_t bm = cur;
-                chain_scan(s, e, best, bm, 1e-12 * (1.0 + cc),
-                           [&](uint32_t m) { return icost(S, s, m) + icost(S, m + 1, e); });
-                if (bm != cur) {
-                    __syncwarp();
-                    if (tid == 0) {
-                        sh.ivs[c] = bm;
-                        sh.ivf[c + 1] = bm + 1;
-                    }
-                    __syncwarp();
-                    changed = true;
+    constexpr uint32_t NW = kThreads / 32;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    bool any = false;
+    for (int sweep = 0; sweep < 32; ++sweep) {
+        bool changed = false;
+        for (uint32_t c = 0; c + 1 < k; ++c) {  // pairwise cuts
+            const uint32_t s = sh.ivf[c], e = sh.ivs[c + 1], cur = sh.ivs[c];
+            const double cc = icost(S, s, cur) + icost(S, cur + 1, e);
+            const double eps = 1e-12 * (1.0 + cc);
+            auto cost = [&](uint32_t m) { return icost(S, s, m) + icost(S, m + 1, e); };
+            const double mn = block_min(sh, s, e, cost);
+            uint32_t bm = cur;
+            if (mn < cc - eps) {
+                if (warp == 0) {
+                    double best = cc;
+                    chain_scan(s, e, best, bm, eps, cost);
+                    if (lane == 0) sh.flag = bm;
                 }
+                __syncthreads();
+                bm = sh.flag;
             }
-            for (uint32_t c = 0; c + 2 < k; ++c) {  // joint cuts over three clusters
-                const uint32_t s = sh.ivf[c], e = sh.ivs[c + 2];
-                const uint32_t c1 = sh.ivs[c], c2 = sh.ivs[c + 1];
-                const double cc = icost(S, s, c1) + icost(S, c1 + 1, c2) + icost(S, c2 + 1, e);
-                const double eps = 1e-12 * (1.0 + cc);
-                double best = cc;
-                uint32_t b1 = c1, b2 = c2;
-                for (uint32_t m1 = s; m1 + 1 < e; ++m1) {
-                    const double left = icost(S, s, m1);
-                    if (left >= best) break;
-                    uint32_t bm = 0xffffffffu;
-                    chain_scan(m1 + 1, e, best, bm, eps, [&](uint32_t m2) {
-                        return left + icost(S, m1 + 1, m2) + icost(S, m2 + 1, e);
-                    });
-                    if (bm != 0xffffffffu) {
-                        b1 = m1;
-                        b2 = bm;
-                    }
+            if (bm != cur) {
+                __syncthreads();
+                if (tid == 0) {
+                    sh.ivs[c] = bm;
+                    sh.ivf[c + 1] = bm + 1;
                 }
-                if (b1 != c1 || b2 != c2) {
-                    __syncwarp();
-                    if (tid == 0) {
-                        sh.ivs[c] = b1;
-                        sh.ivf[c + 1] = b1 + 1;
-                        sh.ivs[c + 1] = b2;
-                        sh.ivf[c + 2] = b2 + 1;
-                    }
-                    __syncwarp();
-                    changed = true;
-                }
+                changed = true;
             }
-            if (!changed) break;
-            any = true;
+            __syncthreads();
         }
-        if (tid == 0) sh.changed = any ? 1u : 0u;
+        for (uint32_t c = 0; c + 2 < k; ++c) {  // joint cuts over three clusters
+            const uint32_t s = sh.ivf[c], e = sh.ivs[c + 2];
+            const uint32_t c1 = sh.ivs[c], c2 = sh.ivs[c + 1];
+            const double cc = icost(S, s, c1) + icost(S, c1 + 1, c2) + icost(S, c2 + 1, e);
+            const double eps = 1e-12 * (1.0 + cc);
+            double R = cc;  // warp 0 owns the record; others read sh.total
+            uint32_t b1 = c1, b2 = c2;
+            for (uint32_t base = s;; base += NW) {
+                // warp q: row m1 = base + q -> its left cost and row minimum
+                const uint32_t m1 = base + warp;
+                double left = __longlong_as_double(0x7ff0000000000000ll), mn = left;
+                if (m1 + 1 < e) {
+                    left = icost(S, s, m1);
+                    for (uint32_t m2 = m1 + 1 + lane; m2 < e; m2 += 32) {
+                        const double v = left + icost(S, m1 + 1, m2) + icost(S, m2 + 1, e);
+                        mn = v < mn ? v : mn;
+                    }
+                    for (int o = 16; o; o >>= 1) {
+                        const double t = __shfl_xor_sync(0xffffffffu, mn, o);
+                        mn = t < mn ? t : mn;
+                    }
+                }
+                if (lane == 0) {
+                    sh.num[warp] = left;
+                    sh.den[warp] = mn;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    uint32_t done = 0;
+                    for (uint32_t q = 0; q < NW; ++q) {
+                        const uint32_t r1 = base + q;
+                        if (r1 + 1 >= e) {
+                            done = 1;
+                            break;
+                        }
+                        const double lq = sh.num[q];
+                        if (lq >= R) {
+                            done = 1;
+                            break;
+                        }
+                        if (sh.den[q] < R - eps) {
+                            uint32_t bm = 0xffffffffu;
+                            chain_scan(r1 + 1, e, R, bm, eps, [&](uint32_t m2) {
+                                return lq + icost(S, r1 + 1, m2) + icost(S, m2 + 1, e);
+                            });
+                            if (bm != 0xffffffffu) {
+                                b1 = r1;
+                                b2 = bm;
+                            }
+                        }
+                    }
+                    if (lane == 0) sh.flag = done;
+                }
+                __syncthreads();
+                const bool done = sh.flag != 0;
+                __syncthreads();
+                if (done) break;
+            }
+            if (warp == 0 && lane == 0) {
+                sh.red_i[0] = b1;
+                sh.red_i[1] = b2;
+            }
+            __syncthreads();
+            b1 = sh.red_i[0];
+            b2 = sh.red_i[1];
+            if (b1 != c1 || b2 != c2) {
+                __syncthreads();
+                if (tid == 0) {
+                    sh.ivs[c] = b1;
+                    sh.ivf[c + 1] = b1 + 1;
+                    sh.ivs[c + 1] = b2;
+                    sh.ivf[c + 2] = b2 + 1;
+                }
+                changed = true;
+            }
+            __syncthreads();
+        }
+        if (!changed) break;
+        any = true;
     }
-    __syncthreads();
-    if (!sh.changed) return false;
+    if (!any) return false;
     // rebuild centroids, counts, assignment from the refined intervals
     for (uint32_t c = tid; c < k; c += kThreads) {
         sh.cent[c] = float(imean(S, sh.ivf[c], sh.ivs[c]));
@@ -465,6 +550,12 @@ __global__ void __launch_bounds__(kThreads) kmeans_groups(QuantParams P) {
         S.pw = reinterpret_cast<double*>(take(size_t(gcols + 1) * 8));
         S.pwv = reinterpret_cast<double*>(take(size_t(gcols + 1) * 8));
         S.pwv2 = reinterpret_cast<double*>(take(size_t(gcols + 1) * 8));
+        if (P.smem_prefix) {  // the interval-cost tables in shared memory
+            extern __shared__ double dsm[];
+            S.pw = dsm;
+            S.pwv = dsm + (gcols + 1);
+            S.pwv2 = dsm + 2 * size_t(gcols + 1);
+        }
         S.assign = reinterpret_cast<uint16_t*>(take(size_t(gcols) * 2));
         S.vals = reinterpret_cast<float*>(take(size_t(gcols) * 4));
         S.wts = reinterpret_cast<float*>(take(size_t(gcols) * 4));
@@ -606,14 +697,33 @@ __global__ void __launch_bounds__(kThreads) kmeans_groups(QuantParams P) {
                 }
                 __syncthreads();
                 uint32_t budget = P.max_iters;
+                long long t0 = clock64(), tl = 0, tr = 0, tm = 0;
                 const uint32_t used = lloyd(S, sh, k, budget, P.tol);
+                uint32_t rounds = 0, iters = used;
+                tl += clock64() - t0;
                 budget -= used < budget ? used : budget;
                 for (int round = 0; round < 64 && budget > 0; ++round) {
+                    t0 = clock64();
                     const bool refined = boundary_refine(S, sh, k);
+                    tr += clock64() - t0;
+                    t0 = clock64();
                     const bool moved = merge_split(S, sh, k);
+                    tm += clock64() - t0;
                     if (!refined && !moved) break;
+                    t0 = clock64();
                     const uint32_t it = lloyd(S, sh, k, budget, P.tol);
+                    tl += clock64() - t0;
+                    ++rounds;
+                    iters += it;
                     budget -= it < budget ? it : budget;
+                }
+                if (P.prof && tid == 0) {  // dev: per-group cycle profile
+                    unsigned long long* q = P.prof + size_t(g) * 6;
+                    q[0] = tl;
+                    q[1] = tr;
+                    q[2] = tm;
+                    q[3] = rounds;
+                    q[4] = iters;
                 }
                 // back to the original order
                 for (uint32_t i = tid; i < n; i += kThreads) {
@@ -646,9 +756,17 @@ __global__ void __launch_bounds__(kThreads) kmeans_groups(QuantParams P) {
 }
 
 cudaError_t launch_kmeans(const QuantParams& p, uint32_t grid, cudaStream_t st) {
-    kmeans_groups<<<grid, kThreads, 0, st>>>(p);
+    const size_t smem = p.smem_prefix ? kmeans_smem_bytes(p.cols / p.groups_per_row) : 0;
+    if (smem) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            kmeans_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    kmeans_groups<<<grid, kThreads, smem, st>>>(p);
     return cudaGetLastError();
 }
+
+size_t kmeans_smem_bytes(uint32_t gcols) { return size_t(gcols + 1) * 3 * 8; }
 
 size_t kmeans_scratch_stride(uint32_t gcols, size_t npow2) {
     auto r = [](size_t b) { return (b + 255) & ~size_t(255); };

@@ -25,9 +25,12 @@ struct QuantParams {
     uint8_t* scratch;        // per-CTA workspace
     size_t scratch_stride;
     size_t npow2;            // sort length (power of two >= group length)
+    int smem_prefix;
+    unsigned long long* prof;  // dev: [groups][6] cycles lloyd/refine/merge, rounds, iterations         // interval-cost prefix tables in dynamic shared memory
 };
 
 cudaError_t launch_kmeans(const QuantParams& p, uint32_t grid, cudaStream_t st);
 size_t kmeans_scratch_stride(uint32_t gcols, size_t npow2);
+size_t kmeans_smem_bytes(uint32_t gcols);  // dynamic smem with smem_prefix
 
 }  // namespace sqz

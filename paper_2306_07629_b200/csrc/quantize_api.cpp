@@ -2,8 +2,11 @@
 // dsq::quantize_channelwise (src/nuq.cpp:673-779) with the same validation
 // order and error codes (WeightMatrix::validate tensor.cpp:12-20,
 // QuantConfig::validate nuq.cpp:24-34, group_size / empty_channel checks).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -68,7 +71,15 @@ extern "C" int dsq_cuda_quantize_channelwise(const float* w, const float* sens,
     if (e != cudaSuccess) return dsq_internal_fail(DSQ_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const uint32_t grid = uint32_t(std::min<size_t>(groups, size_t(sms > 0 ? sms : 1) * 8));
+    // prefix tables in shared memory when they fit; CTAs per SM from the
+    // shared-memory footprint (static ~11 KB + the tables)
+    int smax = 0;
+    cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const size_t pre = sqz::kmeans_smem_bytes(gcols);
+    const bool in_smem = pre + 16 * 1024 <= size_t(smax);
+    const size_t per_cta = (in_smem ? pre : 0) + 12 * 1024;
+    const size_t per_sm = std::max<size_t>(1, std::min<size_t>(8, (size_t(smax) + 1024) / per_cta));
+    const uint32_t grid = uint32_t(std::min<size_t>(groups, size_t(sms > 0 ? sms : 1) * per_sm));
     const size_t stride = sqz::kmeans_scratch_stride(gcols, np);
     DevBuf dw, ds, dm, dc, da, dobj, dmse, dfail, dscr;
     if ((e = dw.alloc(total * 4)) || (e = ds.alloc(total * 4)) ||
@@ -100,8 +111,25 @@ extern "C" int dsq_cuda_quantize_channelwise(const float* w, const float* sens,
     P.scratch = static_cast<uint8_t*>(dscr.p);
     P.scratch_stride = stride;
     P.npow2 = np;
+    P.smem_prefix = in_smem ? 1 : 0;
+    DevBuf dprof;
+    const bool prof = std::getenv("DSQ_KMEANS_PROFILE") != nullptr;  // dev
+    if (prof && dprof.alloc(groups * 6 * 8) == cudaSuccess) {
+        cudaMemset(dprof.p, 0, groups * 6 * 8);
+        P.prof = static_cast<unsigned long long*>(dprof.p);
+    }
     if ((e = sqz::launch_kmeans(P, grid, 0)) || (e = cudaDeviceSynchronize()))
         return dsq_internal_fail(DSQ_E_CUDA, "kmeans_groups: %s", cudaGetErrorString(e));
+    if (P.prof) {
+        std::vector<unsigned long long> h(groups * 6);
+        cudaMemcpy(h.data(), P.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+        double a[5] = {0, 0, 0, 0, 0};
+        for (size_t g = 0; g < groups; ++g)
+            for (int q = 0; q < 5; ++q) a[q] += double(h[g * 6 + q]);
+        std::fprintf(stderr, "kmeans profile (mean per group): lloyd %.0f refine %.0f merge %.0f "
+                     "cycles, rounds %.2f, iterations %.2f (grid %u)\n", a[0] / groups,
+                     a[1] / groups, a[2] / groups, a[3] / groups, a[4] / groups, grid);
+    }
     std::vector<uint8_t> failed(groups);
     std::vector<double> obj(groups), mse(groups);
     if ((e = cudaMemcpy(failed.data(), dfail.p, groups, cudaMemcpyDeviceToHost)) ||
