@@ -344,11 +344,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 yp.append(ys[slot][j].data_ptr())
             one.append(DeviceStack(layers, deps, xp, yp, N.F16))
 
+        y_last = [ys[slot][len(SHAPES) - 1] for slot in range(n_rot)]
+
         def e2e_step(slot):
-            x_dev.copy_(x_host, non_blocking=True)
-            one[slot].run(sp)
-            y_host.copy_(ys[slot][len(SHAPES) - 1], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            one[slot].run_host(x_host.data_ptr(), x_dev.data_ptr(), x_host.numel() * 2,
+                               y_last[slot].data_ptr(), y_host.data_ptr(), y_host.numel() * 2, sp)
 
         for s in range(3):
             e2e_step(s % n_rot)
@@ -365,8 +365,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e = {"value": round(world * bytes_step * n_e2e / el / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": SHAPES[-1][1] * 2,
                "steps": n_e2e, "ms_per_step": round(el / n_e2e * 1e3, 4),
-               "api": "DeviceStack.run (dsq_cuda_stack_run) per decoder-layer step, pinned "
-                      "host x -> device, step output -> pinned host, synchronized per step"}
+               "api": "DeviceStack.run_host (dsq_cuda_stack_run_host) per decoder-layer step: "
+                      "pinned host x -> device, the 7-GEMV stack, step output -> pinned host, "
+                      "stream synchronised every step"}
         # the reference-signature host call, per GEMV (fp32 host x -> fp64 host y,
         # dsq_cuda_matvec_host = fused_dns_matvec(layer, x)), for comparison
         xh = make_x(4096).astype(np.float32)

@@ -208,6 +208,12 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
                           const void* const* xs, void* const* ys, int y_dtype,
                           dsq_cuda_stack** out);
 int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
+/* one decode step from host buffers: copy x_host (x_bytes, pinned for async)
+ * into x_dev (the stack's external input), run the stack, copy y_dev into
+ * y_host, synchronise the stream.  A 0 byte count skips that copy. */
+int dsq_cuda_stack_run_host(dsq_cuda_stack* stack, const void* x_host, void* x_dev,
+                            size_t x_bytes, const void* y_dev, void* y_host, size_t y_bytes,
+                            void* stream);
 int dsq_cuda_stack_destroy(dsq_cuda_stack* stack);
 
 /* ---- tensor parallelism: the all-reduce fused into the stack -- */

@@ -1159,6 +1159,23 @@ extern "C" uint64_t dsq_cuda_stack_trace(dsq_cuda_stack* S, unsigned long long* 
     return n;
 }
 
+// one decode step from host memory: x_host -> x_dev, the stack, y_dev ->
+// y_host, stream synchronised -- the host-buffer form of dsq_cuda_stack_run
+int dsq_cuda_stack_run_host(dsq_cuda_stack* S, const void* x_host, void* x_dev, size_t x_bytes,
+                            const void* y_dev, void* y_host, size_t y_bytes, void* stream) {
+    if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
+    if ((x_bytes && (!x_host || !x_dev)) || (y_bytes && (!y_dev || !y_host)))
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack_run_host: null buffer");
+    cudaSetDevice(S->device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (x_bytes) CUDA_TRY(cudaMemcpyAsync(x_dev, x_host, x_bytes, cudaMemcpyHostToDevice, st));
+    const int rc = dsq_cuda_stack_run(S, stream);
+    if (rc) return rc;
+    if (y_bytes) CUDA_TRY(cudaMemcpyAsync(y_host, y_dev, y_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return DSQ_OK;
+}
+
 int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
     if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
     cudaSetDevice(S->device);

@@ -277,6 +277,13 @@ class DeviceStack:
     def run(self, stream: int = 0) -> None:
         check(lib.dsq_cuda_stack_run(self.handle, stream))
 
+    def run_host(self, x_host: int, x_dev: int, x_bytes: int, y_dev: int, y_host: int,
+                 y_bytes: int, stream: int = 0) -> None:
+        """One step from host buffers (pointers): x_host -> x_dev, run, y_dev ->
+        y_host, synchronised (dsq_cuda_stack_run_host)."""
+        check(lib.dsq_cuda_stack_run_host(self.handle, x_host, x_dev, x_bytes, y_dev, y_host,
+                                          y_bytes, stream))
+
 
 def device_layer(layer: QuantizedLayer, device: int = 0) -> DeviceLayer:
     """Upload once and cache on the layer object (layers are immutable)."""
