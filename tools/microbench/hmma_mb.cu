@@ -94,17 +94,33 @@ __device__ __forceinline__ void span4(const uint4& w, const P16& P, const uint4&
 #define NSPAN 8   // spans resident in smem per warp (cycled)
 // VAR 0: 3-bit SHF shifts; 1: 3-bit IMAD.HI shifts; 2: 4-bit
 template<int VAR, int RT, int XCF = 0>
-__global__ void __launch_bounds__(768) k_hmma(int niter, float* out, Clk* clk, uint32_t seed, uint32_t k16, uint32_t k29, uint32_t k30, uint32_t k31){
+__global__ void __launch_bounds__(768) k_hmma(int niter, float* out, Clk* clk, uint32_t seed, uint32_t k16, uint32_t k29, uint32_t k30, uint32_t k31, int idle = 0){
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // idle "role" warps (the stack kernel's publisher/loader/finisher/CSR
+  // warps): wait on an mbarrier that never completes until the decode warps
+  // are done (mbar_wait's suspend-hint try_wait loop)
+  __shared__ __align__(8) unsigned long long ibar;
+  __shared__ int idone;
+  if (threadIdx.x == 0) { idone = 0; asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&ibar))); }
+  __syncthreads();
+
   const int WPS = VAR == 2 ? 4 : 3;
   (void)WPS;              // words per lane per span per tile
   uint32_t* pk = sm + warp * (NSPAN * RT * WPS * 32);
-  uint32_t* sx = sm + (blockDim.x / 32) * (NSPAN * RT * WPS * 32);   // x: NSPAN * 4 groups * 32 halves
+  uint32_t* sx = sm + (blockDim.x / 32 - idle) * (NSPAN * RT * WPS * 32);   // x: NSPAN * 4 groups * 32 halves
   const int nw = blockDim.x / 32;
-  for (int i = lane; i < NSPAN * RT * WPS * 32; i += 32) { uint32_t h = (i * 2654435761u) ^ seed ^ warp; pk[i] = h; }
+  for (int i = lane; warp < int(blockDim.x / 32) - idle && i < NSPAN * RT * WPS * 32; i += 32) { uint32_t h = (i * 2654435761u) ^ seed ^ warp; pk[i] = h; }
   for (int i = threadIdx.x; i < NSPAN * 128; i += blockDim.x) sx[i] = 0x3c003800u ^ (i & 0x00ff00ff);
   __syncthreads();
+  if (warp >= int(blockDim.x / 32) - idle) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(&ibar);
+    while (*(volatile int*)&idone < int(blockDim.x / 32) - idle) {
+      uint32_t done;
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(a), "r"(0u), "r"(1000000u) : "memory");
+    }
+    return;
+  }
   (void)nw;
   const uint32_t g = lane >> 2, t = lane & 3, n = g & 3;
   P8 P[RT]; P16 Q[RT];
@@ -161,6 +177,7 @@ __global__ void __launch_bounds__(768) k_hmma(int niter, float* out, Clk* clk, u
     }
   }
   if (threadIdx.x==0){ c.c1 = clock64(); c.t1 = gtimer(); if (blockIdx.x==0) *clk = c; }
+  if (lane == 0) atomicAdd(&idone, 1);
   float a = 0.f;
   #pragma unroll
   for (int r = 0; r < RT; ++r) a += d[r][0] + d[r][1] + d[r][2] + d[r][3] + d2[r][0] + d2[r][3];
@@ -173,15 +190,15 @@ int main(){
   printf("device %s SMs %d\n", pr.name, nsm);
   float* out; CK(cudaMalloc(&out, size_t(nsm)*4*1024*sizeof(float)));
   Clk* clk; CK(cudaMalloc(&clk, sizeof(Clk)));
-  auto run = [&](auto kern, const char* name, int var, int rt, int warps, int ctas) -> int {
+  auto run = [&](auto kern, const char* name, int var, int rt, int warps, int ctas, int idle = 0) -> int {
     const int wps = var == 2 ? 4 : 3;
     size_t smem = size_t(warps) * NSPAN * rt * wps * 32 * 4 + NSPAN * 128 * 4;
     if (smem * ctas > 227 * 1024) { printf("%-34s warps %2d ctas %d: smem too big\n", name, warps, ctas); return 0; }
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = nsm * ctas, niter = 20000;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    kern<<<grid, warps*32, smem>>>(100, out, clk, 1, 1u<<16, 1u<<29, 1u<<30, 1u<<31); CK(cudaDeviceSynchronize());
-    cudaEventRecord(e0); kern<<<grid, warps*32, smem>>>(niter, out, clk, 2, 1u<<16, 1u<<29, 1u<<30, 1u<<31); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    kern<<<grid, (warps+idle)*32, smem>>>(100, out, clk, 1, 1u<<16, 1u<<29, 1u<<30, 1u<<31, idle); CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0); kern<<<grid, (warps+idle)*32, smem>>>(niter, out, clk, 2, 1u<<16, 1u<<29, 1u<<30, 1u<<31, idle); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     Clk h; cudaMemcpy(&h, clk, sizeof(Clk), cudaMemcpyDeviceToHost);
     const double ghz = double(h.c1-h.c0)/double(h.t1-h.t0);
@@ -198,6 +215,7 @@ int main(){
     run(k_hmma<5,2,1>, "3b product RT2 xcf", 5, 2, warps, 1);
     run(k_hmma<6,2,1>, "3b product+imad RT2 xcf", 6, 2, warps, 1);
     run(k_hmma<7,1,1>, "3b stack span-pair (one acc/unit)", 7, 1, warps, 1);
+    run(k_hmma<7,1,1>, "3b span-pair + 7 idle role warps", 7, 1, warps, 1, 7);
     run(k_hmma<8,1,1>, "3b span-pair dual acc", 8, 1, warps, 1);
 
   }
