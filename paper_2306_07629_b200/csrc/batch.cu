@@ -82,6 +82,10 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batch_gemv(const __grid_cons
     const uint32_t s1 = min(p.ns, s0 + p.spans_per_slice);
     const uint32_t c0 = s0 * kSpanCols;
     const uint32_t ccount = min(p.cols, s1 * kSpanCols) - min(p.cols, c0);
+    // x and the partial buffer may belong to the previous launch on this
+    // stream (programmatic dependent launch): wait for it first
+    pdl_trigger();
+    pdl_wait();
     // stage the slice's x for all 8*NB B-columns (zero beyond B and cols),
     // 16 bytes per load (x rows are 16-byte aligned, cols % 8 == 0)
     {
@@ -197,6 +201,8 @@ __global__ void batch_finish(const float* __restrict__ part, uint32_t kslices, u
                              const uint32_t* __restrict__ csr, const uint16_t* __restrict__ x,
                              uint32_t x_stride, void* y, uint32_t y_stride, int y_f16,
                              int with_dense, int with_csr) {
+    pdl_trigger();
+    pdl_wait();  // the partials of the preceding batch_gemv
     const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (id >= size_t(rows) * B) return;
     const uint32_t r = uint32_t(id / B), b = uint32_t(id % B);
@@ -231,6 +237,24 @@ __global__ void batch_finish(const float* __restrict__ part, uint32_t kslices, u
         static_cast<__half*>(y)[size_t(b) * y_stride + r] = __float2half_rn(s);
     else
         static_cast<float*>(y)[size_t(b) * y_stride + r] = s;
+}
+
+// launch with programmatic stream serialization (the kernel calls pdl_wait
+// before touching data of the previous launch), so back-to-back products
+// overlap one kernel's tail with the next one's launch
+template <class K, class... A>
+cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 size_t batch_smem_bytes(uint32_t B, uint32_t spans_per_slice) {
@@ -269,15 +293,14 @@ cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut
         if (smem > 48 * 1024)
             e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
-        k<<<groups * kslices, kBatchWarps * 32, smem, st>>>(p);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = launch_pdl(k, dim3(groups * kslices), dim3(kBatchWarps * 32), smem, st, p)) !=
+            cudaSuccess)
+            return e;
     }
     const size_t n = size_t(rows) * B;
-    batch_finish<<<uint32_t((n + 255) / 256), 256, 0, st>>>(part, kslices, p.tiles16, rows, B,
-                                                            row_ptr, csr, x, x_stride, y,
-                                                            y_stride, y_f16 ? 1 : 0, with_dense,
-                                                            with_csr);
-    return cudaGetLastError();
+    return launch_pdl(batch_finish, dim3(uint32_t((n + 255) / 256)), dim3(256), 0, st, part,
+                      kslices, p.tiles16, rows, B, row_ptr, csr, x, x_stride, y, y_stride,
+                      y_f16 ? 1 : 0, with_dense, with_csr);
 }
 
 }  // namespace sqz
