@@ -505,6 +505,25 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
     for _ in range(2):
         s_warm.run(sp)
     torch.cuda.synchronize()
+    # validate the fused reduce on this machine before timing it: no
+    # watchdog event, and every rank holds the same reduced outputs (the
+    # last step's o and down); otherwise all ranks fall back to replicas
+    ok = 1
+    try:
+        ctx.check()
+    except Exception as e:
+        print(f"rank {rank}: tp watchdog: {e}", file=sys.stderr)
+        ok = 0
+    slot = (args.warmup - 1) % n_rot
+    sig = torch.stack([ys[slot][3].to(torch.int64).sum(), ys[slot][6].to(torch.int64).sum()])
+    sigs = [torch.zeros_like(sig) for _ in range(world)]
+    dist.all_gather(sigs, sig)
+    if any(not torch.equal(g, sigs[0]) for g in sigs):
+        ok = 0
+    flag = torch.tensor([ok], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if not int(flag.item()):
+        raise TPUnavailable("fused TP reduce failed validation (watchdog or rank mismatch)")
     setup_s = time.time() - t_setup
     sampler = ClockSampler(local_rank)
     sampler.start()
