@@ -354,6 +354,17 @@ typedef struct dsq_quant_config {  /* dsq::QuantConfig (nuq.hpp:26-37) */
 enum { DSQ_CODEBOOK_WEIGHTED_KMEANS = 0, DSQ_CODEBOOK_UNWEIGHTED_KMEANS = 1, DSQ_CODEBOOK_RTN = 2 };
 /* w, sens: [rows*cols]; mask: [rows*cols] or NULL; centroids out:
  * [rows * groups_per_row * 2^bits]; assign out: [rows*cols] */
+/* dsq::decompose (reference src/dns.cpp:73-145) on the GPU: the mask of the
+ * ceil(sensitive_fraction*N) most sensitive weights plus the
+ * ceil(outlier_fraction*N) largest magnitudes among the rest (ties: lower
+ * row-major index), and their CSR (original values).  row_ptr [rows+1];
+ * col_idx / values sized >= nnz (*nnz is set even when the capacity is too
+ * small).  Same validation and error codes as the reference. */
+int dsq_cuda_decompose(const float* w, const float* sens, uint32_t rows, uint32_t cols,
+                       const dsq_quant_config* cfg, int device, uint8_t* mask, uint32_t* row_ptr,
+                       uint16_t* col_idx, float* values, uint64_t nnz_cap, uint64_t* nnz,
+                       uint32_t* sensitive_count, uint32_t* outlier_count, float* t_min,
+                       float* t_max);
 int dsq_cuda_quantize_channelwise(const float* w, const float* sens, const uint8_t* mask,
                                   uint32_t rows, uint32_t cols, const dsq_quant_config* cfg,
                                   int method, int device, float* centroids, uint16_t* assign,

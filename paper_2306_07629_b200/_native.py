@@ -175,6 +175,11 @@ PROTOTYPES = {
                                                 C.c_uint32, C.POINTER(QuantConfig), C.c_int,
                                                 C.c_int, C.c_void_p, C.c_void_p,
                                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "dsq_cuda_decompose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32,
+                                     C.POINTER(QuantConfig), C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "dsq_gemv_cost": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
                                 C.POINTER(HwProfile), C.POINTER(LayerCost)]),
 }

@@ -125,3 +125,74 @@ def test_validation_matches_reference(reference, case):
     rc = reference.quantize_channelwise(w, sens, cfg["bits"], cfg["group_size"],
                                         cfg["max_iters"], cfg["tol"])[0]
     assert e.value.code == rc != 0
+
+
+# ---- the whole quantize_layer pipeline (decompose K10 + k-means K9 + pack) ----
+
+def _ref_layer_arrays(reference, w, sens, bits, sf, of, top_k=10):
+    rl = reference.quantize(w, sens, w.shape[0], w.shape[1], bits, sf, of, top_k)
+    a = rl.arrays()
+    return (a["luts"], a["payload"], a["row_ptr"], a["col_idx"], a["values"]), \
+        float(reference.lib.ref_avg_bits(rl.h))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,sf,of,kind", [
+    (3, 0.0005, 0.004, "normal"),       # the pipeline defaults (0.45%)
+    (4, 0.0005, 0.004, "normal"),
+    (3, 0.01, 0.02, "ties"),            # equal magnitudes: index tie-break
+    (3, 0.02, 0.01, "zero_sens"),       # all-zero sensitivity: index tie-break
+    (2, 0.0, 0.05, "sparse_sens"),
+    (3, 0.05, 0.0, "normal"),
+])
+def test_quantize_layer_matches_reference(torch, reference, bits, sf, of, kind):
+    from paper_2306_07629_b200.quantize import quantize_layer
+    w, sens = _case(16, 512, seed=bits + int(1000 * sf), kind=kind)
+    (luts, payload, row_ptr, col_idx, values), avg = _ref_layer_arrays(
+        reference, w, sens, bits, sf, of)
+    layer, stats = quantize_layer(w, sens, QuantConfig(bits=bits, sensitive_fraction=sf,
+                                                       outlier_fraction=of))
+    np.testing.assert_array_equal(np.asarray(layer.packed.luts, np.float32).view(np.uint32),
+                                  luts.view(np.uint32))
+    np.testing.assert_array_equal(np.asarray(layer.packed.payload, np.uint8), payload)
+    nnz = int(row_ptr[-1])
+    np.testing.assert_array_equal(np.asarray(layer.sparse.row_ptr, np.uint32), row_ptr)
+    np.testing.assert_array_equal(np.asarray(layer.sparse.col_idx, np.uint16), col_idx[:nnz])
+    np.testing.assert_array_equal(np.asarray(layer.sparse.values, np.float32).view(np.uint32),
+                                  values[:nnz].view(np.uint32))
+    assert stats["avg_bits"] == avg
+    assert stats["sensitive_count"] + stats["outlier_count"] == nnz
+
+
+@pytest.mark.gpu
+def test_quantize_layer_llama_shape_and_device_product(torch, reference, oracle):
+    """A 4096-column layer quantized on the GPU equals the reference's and
+    runs through the hot path (the fused product against the oracle)."""
+    from oracle.oracle import make_x
+    from paper_2306_07629_b200 import fused_dns_matvec
+    from paper_2306_07629_b200.quantize import quantize_layer
+    w, sens = _case(64, 4096, seed=5)
+    (luts, payload, row_ptr, *_), _ = _ref_layer_arrays(reference, w, sens, 3, 0.0005, 0.004)
+    layer, _ = quantize_layer(w, sens, QuantConfig(bits=3))
+    assert np.array_equal(np.asarray(layer.packed.payload, np.uint8), payload)
+    assert np.array_equal(np.asarray(layer.packed.luts, np.float32), luts)
+    x = make_x(4096, seed=1).astype(np.float32)
+    y = fused_dns_matvec(layer, x)
+    ref = reference.quantize(w, sens, 64, 4096, 3, 0.0005, 0.004).matvec("fused", x)
+    assert np.abs(y - ref).max() <= np.abs(ref).max() * 1e-3
+
+
+@pytest.mark.parametrize("case", ["overflow", "wide"])
+def test_decompose_validation(case):
+    from paper_2306_07629_b200.quantize import decompose
+    if case == "overflow":  # ceil(0.05*4)+ceil(0.05*4) = 2 < 4 ok; 2x2 -> 1+1 < 4; 1x1 -> 2 >= 1
+        w, s = np.ones((1, 1), np.float32), np.ones((1, 1), np.float32)
+        code = 12  # errc::fraction_overflow
+        cfg = QuantConfig(sensitive_fraction=0.05, outlier_fraction=0.05)
+    else:
+        w, s = np.ones((1, 65536), np.float32), np.ones((1, 65536), np.float32)
+        code = 5  # errc::dimension_overflow
+        cfg = QuantConfig()
+    with pytest.raises(N.DsqError) as e:
+        decompose(w, s, cfg)
+    assert e.value.code == code
