@@ -18,6 +18,7 @@
 // reproduces dsq::Error and the CLI exit-code mapping (tools/dsq.cpp:399-411).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -134,6 +135,86 @@ std::vector<double> csr_part_matvec(const Layer& l, const std::vector<float>& x)
 inline uint64_t bytes_touched_estimate(uint32_t rows, uint32_t cols, uint32_t bits,
                                        uint32_t group_size, uint64_t nnz) {
     return dsq_bytes_touched_estimate(rows, cols, bits, group_size, nnz);
+}
+
+// ---- the producer side on the GPU, with the caller's reference types ------
+
+template <class Cfg>
+dsq_quant_config quant_config(const Cfg& c) {  // dsq::QuantConfig (nuq.hpp:26-37)
+    dsq_quant_config q{};
+    q.bits = c.bits;
+    q.sensitive_fraction = c.sensitive_fraction;
+    q.outlier_fraction = c.outlier_fraction;
+    q.group_size = c.group_size;
+    q.kmeans_max_iters = c.kmeans_max_iters;
+    q.kmeans_tol = c.kmeans_tol;
+    q.seed = c.seed;
+    return q;
+}
+
+// == dsq::quantize_channelwise(matrix, sens, cfg, mask, method) (nuq.hpp:106-110);
+// Result = dsq::ChannelwiseResult, method = int(dsq::CodebookMethod)
+template <class Result, class Matrix, class Cfg>
+Result quantize_channelwise(const Matrix& m, const std::vector<float>& sens, const Cfg& cfg,
+                            const std::vector<uint8_t>& mask = {}, int method = 0,
+                            int device = 0) {
+    const dsq_quant_config q = quant_config(cfg);
+    const uint32_t k = 1u << cfg.bits;
+    const uint32_t gpr = cfg.group_size ? m.cols / cfg.group_size : 1;
+    std::vector<float> cent(size_t(m.rows) * gpr * k);
+    Result r;
+    r.assignment.resize(size_t(m.rows) * m.cols);
+    double obj = 0, mse = 0;
+    if (sens.size() != m.values.size()) throw Error(DSQ_E_SHAPE_MISMATCH, "sensitivity shape mismatch");
+    if (!mask.empty() && mask.size() != m.values.size())
+        throw Error(DSQ_E_SHAPE_MISMATCH, "mask shape mismatch");
+    check(dsq_cuda_quantize_channelwise(m.values.data(), sens.data(),
+                                        mask.empty() ? nullptr : mask.data(), m.rows, m.cols, &q,
+                                        method, device, cent.data(), r.assignment.data(), &obj,
+                                        &mse));
+    r.groups_per_row = gpr;
+    r.codebooks.resize(size_t(m.rows) * gpr);
+    for (size_t g = 0; g < r.codebooks.size(); ++g)
+        r.codebooks[g].centroids.assign(cent.begin() + g * k, cent.begin() + (g + 1) * k);
+    r.weighted_objective = obj;
+    r.unweighted_mse_sum = mse;
+    return r;
+}
+
+// == dsq::decompose(matrix, sens, cfg) (dns.hpp:44-49); Decomp = dsq::Decomposition
+template <class Decomp, class Matrix, class Cfg>
+Decomp decompose(const Matrix& m, const std::vector<float>& sens, const Cfg& cfg, int device = 0) {
+    const dsq_quant_config q = quant_config(cfg);
+    const size_t n = m.values.size();
+    if (sens.size() != n) throw Error(DSQ_E_SHAPE_MISMATCH, "sensitivity shape mismatch");
+    Decomp d;
+    d.mask.assign(n, 0);
+    d.sparse.rows = m.rows;
+    d.sparse.cols = m.cols;
+    d.sparse.row_ptr.assign(size_t(m.rows) + 1, 0);
+    uint64_t nnz = 0;
+    // first call sizes the CSR (capacity 0 -> DSQ_E_INVALID_ARGUMENT with nnz set)
+    const size_t cap = size_t(std::ceil(cfg.sensitive_fraction * double(n))) +
+                       size_t(std::ceil(cfg.outlier_fraction * double(n)));
+    d.sparse.col_idx.resize(cap);
+    d.sparse.values.resize(cap);
+    uint32_t sc = 0, oc = 0;
+    float lo = 0, hi = 0;
+    check(dsq_cuda_decompose(m.values.data(), sens.data(), m.rows, m.cols, &q, device,
+                             d.mask.data(), d.sparse.row_ptr.data(),
+                             cap ? d.sparse.col_idx.data() : nullptr,
+                             cap ? d.sparse.values.data() : nullptr, cap, &nnz, &sc, &oc, &lo,
+                             &hi));
+    d.sparse.col_idx.resize(nnz);
+    d.sparse.values.resize(nnz);
+    d.dense = m;
+    for (size_t i = 0; i < n; ++i)
+        if (d.mask[i]) d.dense.values[i] = 0.0f;
+    d.t_min = lo;
+    d.t_max = hi;
+    d.sensitive_count = sc;
+    d.outlier_count = oc;
+    return d;
 }
 
 }  // namespace sqz

@@ -10,7 +10,9 @@
 #include <cstdio>
 #include <vector>
 
+#include "dsq/dns.hpp"
 #include "dsq/kernels.hpp"
+#include "dsq/nuq.hpp"
 #include "dsq/pipeline.hpp"
 #include "dsq/sensitivity.hpp"
 #include "dsq_cuda.hpp"
@@ -90,6 +92,27 @@ int main() {
         } catch (const sqz::Error& e) {
             if (e.errc() != int(errc::shape_mismatch)) return fail("errc mapping", e.errc());
         }
+        // the producer side: decompose + quantize_channelwise on the GPU with
+        // the reference's types, bit-identical to the reference's
+        const Decomposition dr = decompose(w, s.values, opt.cfg);
+        const Decomposition dg = sqz::decompose<Decomposition>(w, s.values, opt.cfg);
+        if (dg.mask != dr.mask || dg.sparse.row_ptr != dr.sparse.row_ptr ||
+            dg.sparse.col_idx != dr.sparse.col_idx || dg.sparse.values != dr.sparse.values ||
+            dg.dense.values != dr.dense.values || dg.t_min != dr.t_min || dg.t_max != dr.t_max ||
+            dg.sensitive_count != dr.sensitive_count || dg.outlier_count != dr.outlier_count)
+            return fail("decompose", 0);
+        const ChannelwiseResult cr = quantize_channelwise(w, s.values, opt.cfg, dr.mask);
+        const ChannelwiseResult cg =
+            sqz::quantize_channelwise<ChannelwiseResult>(w, s.values, opt.cfg, dr.mask);
+        if (cg.assignment != cr.assignment || cg.codebooks.size() != cr.codebooks.size() ||
+            cg.weighted_objective != cr.weighted_objective ||
+            cg.unweighted_mse_sum != cr.unweighted_mse_sum)
+            return fail("quantize_channelwise", 0);
+        for (size_t g = 0; g < cr.codebooks.size(); ++g)
+            if (cg.codebooks[g].centroids != cr.codebooks[g].centroids)
+                return fail("codebook", double(g));
+        std::printf("decompose + quantize_channelwise: bit-identical (%u extracted)\n",
+                    dr.sparse.row_ptr.back());
     } catch (const sqz::Error& e) {
         std::printf("sqz::Error status %d: %s\n", e.status(), e.what());
         return 2;
