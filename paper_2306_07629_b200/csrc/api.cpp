@@ -212,7 +212,7 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, 
 }
 
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
-               uint32_t& gseg_cap) {
+               uint32_t& gseg_cap, uint32_t nbatch = 1) {
     int dev = 0, smax = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -232,7 +232,9 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.off_desc = uint32_t(off);
     off += 8 * 128;     // descriptor cache (stack.cu)
     sp.off_x = uint32_t(off);
-    sp.x_bytes = uint32_t(al(size_t(max_ns) * kSpanCols * 2, 128));
+    sp.nbatch = nbatch;
+    sp.xvec = uint32_t(al(size_t(max_ns) * kSpanCols * 2, 128) / 2);  // halves per vector
+    sp.x_bytes = uint32_t(size_t(sp.xvec) * 2 * nbatch);
     off += 2 * size_t(sp.x_bytes);
     sp.off_lut = uint32_t(off);
     sp.lut_bytes = uint32_t(al(size_t(max_rows) * tile_lut_words(bits) * 4, 128));
@@ -248,10 +250,10 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     off += 2 * size_t(sp.hb_words) * 4;
     sp.off_part = uint32_t(off);
     sp.part_rows = std::max<uint32_t>(max_rows, kTileRows);
-    off = al(off + 2 * size_t(sp.part_rows) * sp.consumers * 4, 128);
+    off = al(off + 2 * size_t(nbatch) * sp.part_rows * sp.consumers * 4, 128);
     sp.off_seg = uint32_t(off);
     sp.seg_cap = sp.csr_cap + 128;  // one float per staged entry position (+ a round)
-    off += 2 * size_t(sp.seg_cap) * 4;
+    off += 2 * size_t(nbatch) * sp.seg_cap * 4;
     gseg_cap = max_nnz > sp.csr_cap - 4 ? uint32_t(al(max_nnz + 256, 4)) : 0;
     sp.off_ring = uint32_t(al(off, 1024));
     // the rest is the consumers' private rings: 2 slots per consumer warp,
@@ -305,6 +307,9 @@ struct dsq_cuda_layer {
     StackParams sp1{};                      // single-layer stack plan
     uint32_t* stack_counters = nullptr;     // [2]
     float* gseg1 = nullptr;
+    StackParams sp2{};                      // batch-2 single-layer stack plan (lazy)
+    bool sp2_ready = false;
+    float* gseg2 = nullptr;
     cudaStream_t stream = nullptr;
     float* batch_part = nullptr;            // batched-product slice partials (lazy)
     uint32_t batch_kslices = 0, batch_spans = 0;
@@ -702,6 +707,7 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (L->stream) cudaStreamDestroy(L->stream);
     if (L->dense_w) cudaFree(L->dense_w);
     if (L->batch_part) cudaFree(L->batch_part);
+    if (L->gseg2) cudaFree(L->gseg2);
     if (L->arena) cudaFree(L->arena);
     delete L;
     return DSQ_OK;
@@ -773,6 +779,54 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
     auto* L = const_cast<dsq_cuda_layer*>(Lc);
     if (!L || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     if (batch < 1 || batch > 16) return fail(DSQ_E_INVALID_ARGUMENT, "batch must be 1..16");
+    if (batch == 2 && L->rec_layout && (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
+        x_dtype == DSQ_F16 && (y_dtype == DSQ_F32 || y_dtype == DSQ_F16) &&
+        !(reinterpret_cast<uintptr_t>(x) & 15u) && L->cols % 8 == 0) {
+        // K7 with two activation vectors in one launch: both share every
+        // decoded weight fragment (the free HMMA B columns 4..7)
+        {
+            std::lock_guard<std::mutex> lk(L->mu);
+            if (!L->sp2_ready) {
+                uint32_t gcap = 0;
+                StackPlanLayer pl{L->rows, L->cols, L->tiles, L->ns,
+                                  max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
+                int prc = plan_stack(&pl, 1, L->num_sms, L->bits, L->sp2, gcap, 2);
+                if (prc) return prc;
+                if (gcap)
+                    CUDA_TRY(cudaMalloc(&L->gseg2, size_t(L->num_sms) * 2 * 2 * gcap * 4 + 4));
+                StackParams& q = L->sp2;
+                const StackLayerDesc& d1 = L->sp1.inl[0];
+                StackLayerDesc& d = q.inl[0];
+                d.idx = d1.idx;
+                d.lut = d1.lut;
+                d.row_ptr = d1.row_ptr;
+                d.csr = d1.csr;
+                d.csr_rng = d1.csr_rng;
+                d.csr_heads = d1.csr_heads;
+                d.dep = kNoDep;
+                d.reduce_ord = kNoDep;
+                q.counters = L->sp1.counters;
+                q.gseg = L->gseg2;
+                q.gseg_cap = gcap;
+                L->sp2_ready = true;
+            }
+        }
+        StackParams sp = L->sp2;
+        StackLayerDesc& d = sp.inl[0];
+        d.x = static_cast<const uint16_t*>(x);
+        d.y = y;
+        d.y_f16 = y_dtype == DSQ_F16 ? 1u : 0u;
+        if (kernel == DSQ_KERNEL_LUT) {  // LUT part only: empty CSR
+            d.row_ptr = L->zero_rp;
+            d.csr_rng = L->zero_rng;
+        }
+        sp.x_bstride = L->cols;
+        sp.y_bstride = L->rows;
+        sp.n_layers = 1;
+        sp.layers = nullptr;
+        CUDA_TRY(launch_stack(sp, st, pdl));
+        return DSQ_OK;
+    }
     if (batch > 1) return gemv_batch(L, kernel, x, x_dtype, y, y_dtype, batch, st);
     if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)
         return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);

@@ -190,7 +190,7 @@ __device__ __forceinline__ void csr_stream(uint32_t ea, uint32_t e0, uint32_t e1
     }
 }
 
-template <int BITS, int NC>
+template <int BITS, int NC, int NB>
 __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     stack_gemv(const __grid_constant__ StackParams p) {
     constexpr uint32_t LW = BITS == 3 ? 4u : 8u;   // LUT words per tile row
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     // the partial tables start at zero; the finisher re-zeroes what it reads
     {
         float* part = reinterpret_cast<float*>(sm + p.off_part);
-        for (uint32_t i = threadIdx.x; i < 2 * NC * p.part_rows; i += blockDim.x) part[i] = 0.f;
+        for (uint32_t i = threadIdx.x; i < 2 * NB * NC * p.part_rows; i += blockDim.x) part[i] = 0.f;
     }
     __syncthreads();
 
@@ -291,13 +291,22 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             // zero padding to the span count), completion on xfull[b]
             auto stage_x = [&]() {
                 const uint32_t body = (d.cols / 8) * 16;  // bytes
-                for (uint32_t i = body / 2 + lane; i < d.ns * kSpanCols; i += 32)
-                    reinterpret_cast<uint16_t*>(xb)[i] = i < d.cols ? ld_cg_u16(d.x + i) : uint16_t(0);
+#pragma unroll
+                for (int v = 0; v < NB; ++v) {  // batch vector v at xb + v * xvec halves
+                    uint16_t* xv = reinterpret_cast<uint16_t*>(xb) + v * p.xvec;
+                    const uint16_t* gx = d.x + size_t(v) * p.x_bstride;
+                    for (uint32_t i = body / 2 + lane; i < d.ns * kSpanCols; i += 32)
+                        xv[i] = i < d.cols ? ld_cg_u16(gx + i) : uint16_t(0);
+                }
                 __syncwarp();
                 if (lane == 0) {
                     fence_proxy_async_global();
-                    mbar_arrive_expect_tx(&xfull[b], body);
-                    if (body) bulk_g2s_plain(xb, d.x, body, &xfull[b]);
+                    mbar_arrive_expect_tx(&xfull[b], NB * body);
+                    if (body)
+#pragma unroll
+                        for (int v = 0; v < NB; ++v)
+                            bulk_g2s_plain(reinterpret_cast<uint16_t*>(xb) + v * p.xvec,
+                                           d.x + size_t(v) * p.x_bstride, body, &xfull[b]);
                 }
             };
             if (d.dep == kNoDep) stage_x();  // external input: no wait at all
@@ -359,10 +368,12 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         if (f == 0 && lane == 0) DSQ_TRACE(l, kTrAllDense);
         // the CSR scan results (position-indexed, see csr_stream)
         const uint32_t ea = sd.e0 & ~3u;
-        const float* S = sd.e1 - sd.e0 <= p.csr_cap - 4
-                             ? reinterpret_cast<const float*>(sm + p.off_seg) + size_t(b) * p.seg_cap
-                             : p.gseg + (size_t(cta) * 2 + b) * p.gseg_cap;
-        float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * NC;
+        const bool staged_csr = sd.e1 - sd.e0 <= p.csr_cap - 4;
+        const float* S = staged_csr
+                             ? reinterpret_cast<const float*>(sm + p.off_seg) + size_t(b) * NB * p.seg_cap
+                             : p.gseg + (size_t(cta) * 2 + b) * NB * p.gseg_cap;
+        const uint32_t s_vec = staged_csr ? p.seg_cap : p.gseg_cap;  // between batch vectors
+        float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * NB * p.part_rows * NC;
         const bool tp = d.reduce_ord != kNoDep;
         const uint32_t par = tp ? (p.tp_base + d.reduce_ord) & 1u : 0u;
         for (uint32_t i = 32 * f + lane; i < sh.nt * kTileRows; i += 32 * kFin) {
@@ -372,10 +383,27 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 s += part[w * p.part_rows + i];
                 part[w * p.part_rows + i] = 0.f;
             }
+            float s1 = 0.f;  // batch vector 1 (NB == 2)
+            if constexpr (NB == 2) {
+                float* part1 = part + NC * p.part_rows;
+#pragma unroll
+                for (uint32_t w = 0; w < NC; ++w) {
+                    s1 += part1[w * p.part_rows + i];
+                    part1[w * p.part_rows + i] = 0.f;
+                }
+            }
             if (i >= nrows) continue;  // padding rows of the last tile
             const uint32_t a = rp[i] - ea, e = rp[i + 1] - ea;
-            for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j)
+            for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j) {
                 s += S[j * 128 + min(e - 1 - j * 128, 127u)];
+                if constexpr (NB == 2) s1 += S[s_vec + j * 128 + min(e - 1 - j * 128, 127u)];
+            }
+            if constexpr (NB == 2) {
+                if (d.y_f16)
+                    static_cast<__half*>(d.y)[p.y_bstride + r0 + i] = __float2half_rn(s1);
+                else
+                    static_cast<float*>(d.y)[p.y_bstride + r0 + i] = s1;
+            }
             if (tp) {
                 // a partial sum: hand it to every rank (own included) at slot
                 // [parity][this rank][row] as one 64-bit word {value, tag} --
@@ -484,9 +512,14 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                                         : sd.d.csr_heads;
             const uint32_t hbase = staged ? ((e0 >> 5) & ~3u) : 0u;
             const uint32_t hlast = staged ? p.hb_words - 2 : ((e1 + 31) >> 5) + 1;
-            float* S = staged ? reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * p.seg_cap
-                              : p.gseg + (size_t(cta) * 2 + b) * p.gseg_cap;
-            if (e1 > e0) csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh, S, cw, kCsrWarps, lane);
+            float* S = staged ? reinterpret_cast<float*>(sm + p.off_seg) + size_t(b) * NB * p.seg_cap
+                              : p.gseg + (size_t(cta) * 2 + b) * NB * p.gseg_cap;
+            if (e1 > e0) {
+#pragma unroll
+                for (int v = 0; v < NB; ++v)
+                    csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh + v * p.xvec,
+                               S + v * (staged ? p.seg_cap : p.gseg_cap), cw, kCsrWarps, lane);
+            }
             __syncwarp();
             if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrDone);
             if (lane == 0) mbar_arrive(&pfull[b]);
@@ -501,7 +534,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     pdl_wait();
     pdl_trigger();
     const uint32_t cw = warp;
-    const uint32_t xoff = tile_x_offset(lane);     // this lane's B-column x halves
+    // this lane's B-column x halves (NB == 2: B columns 4..7, lanes 16..31,
+    // read batch vector 1)
+    const uint32_t xoff = tile_x_offset(lane) + (NB == 2 ? (lane >> 4) * p.xvec : 0u);
     const uint32_t trow = (lane >> 2) & 3u;         // tile row of this lane
     const uint64_t policy = policy_evict_first();
     // this warp's weight stream: its unit range of every layer, in chunks of
@@ -577,7 +612,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrXReady);
         const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_bytes);
         const uint32_t* luts = reinterpret_cast<const uint32_t*>(sm + p.off_lut + b * p.lut_bytes);
-        float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * p.part_rows * NC;
+        float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * NB * p.part_rows * NC;
 
         // dense units: warp cw owns the contiguous unit range [u0, u1) of the
         // CTA share (tile-major: unit u = (tile u / NS, span u % NS)), which
@@ -591,8 +626,15 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
         auto flush = [&]() {
             if (cur_tile != 0xffffffffu) {
-                const float v = tile_rows_reduce(d0, d1, lane);
-                if ((lane & 3) == 0 && lane < 16) part[cw * p.part_rows + cur_tile * kTileRows + trow] += v;
+                if constexpr (NB == 1) {
+                    const float v = tile_rows_reduce(d0, d1, lane);
+                    if ((lane & 3) == 0 && lane < 16) part[cw * p.part_rows + cur_tile * kTileRows + trow] += v;
+                } else {  // vector 0 in lanes 4i, vector 1 in lanes 4i + 2
+                    const float v = tile_rows_reduce2(d0, d1, lane);
+                    if ((lane & 1) == 0 && lane < 16)
+                        part[((lane >> 1) & 1u) * NC * p.part_rows + cw * p.part_rows +
+                             cur_tile * kTileRows + trow] += v;
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) d0[k] = d1[k] = 0.f;
             }
@@ -723,14 +765,15 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static bool attr_done[4][64] = {};
+    static bool attr_done[8][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     const int ci = p.consumers == 8 ? 0 : 1;
-    const int bi = (p.bits == 3 ? 0 : 1) * 2 + ci;
+    const int bi = (p.nbatch == 2 ? 4 : 0) + (p.bits == 3 ? 0 : 1) * 2 + ci;
     using K = void (*)(StackParams);
-    static const K kerns[4] = {stack_gemv<3, 8>, stack_gemv<3, 16>, stack_gemv<4, 8>,
-                               stack_gemv<4, 16>};
+    static const K kerns[8] = {stack_gemv<3, 8, 1>,  stack_gemv<3, 16, 1>, stack_gemv<4, 8, 1>,
+                               stack_gemv<4, 16, 1>, stack_gemv<3, 8, 2>,  stack_gemv<3, 16, 2>,
+                               stack_gemv<4, 8, 2>,  stack_gemv<4, 16, 2>};
     const K kern = kerns[bi];
     if (dev < 0 || dev >= 64 || !attr_done[bi][dev]) {
         int max_optin = 0;

@@ -96,6 +96,13 @@ struct StackParams {
     uint32_t off_part, part_rows;    // two [consumers][part_rows] dense-partial buffers
     uint32_t off_seg, seg_cap;       // two CSR scan-result buffers (floats, position-indexed)
     uint32_t smem_bytes;
+    // batch 2 (single-layer gemv): the two activation vectors share every
+    // decoded A fragment -- vector b feeds the HMMA B columns 4b..4b+3, which
+    // the block-diagonal map leaves free at batch 1.  x buffers, partial
+    // tables and CSR scan buffers hold nbatch vectors each.
+    uint32_t nbatch;                 // 1 or 2
+    uint32_t xvec;                   // halves between the vectors in an smem x buffer
+    uint32_t x_bstride, y_bstride;   // elements between the vectors in global x / y
     // tensor parallelism (world > 1): the partial y of a reduce layer is
     // summed over the ranks' CTAs with the same index over peer memory.
     // recv = [2 parities][world][max_rows] {fp32 value, u32 tag} words per

@@ -170,6 +170,18 @@ __device__ __forceinline__ float tile_rows_reduce(const float (&d0)[4], const fl
     return v;
 }
 
+// the same for two batch vectors (B columns 0-3 = vector 0, 4-7 = vector 1):
+// row i of vector 0 lands in lane 4i, of vector 1 in lane 4i + 2
+__device__ __forceinline__ float tile_rows_reduce2(const float (&d0)[4], const float (&d1)[4],
+                                                   uint32_t lane) {
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const float c0 = d0[0] + d1[0], c1 = d0[1] + d1[1], c2 = d0[2] + d1[2], c3 = d0[3] + d1[3];
+    float v = (t & 1) == 0 ? (g < 4 ? c0 : c1) : (g < 4 ? c2 : c3);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    return v;
+}
+
 // x halves a lane feeds into B: 8 halves at this offset within the span and
 // 8 more at +128 (piece 4n + t, n = B column)
 __device__ __forceinline__ uint32_t tile_x_offset(uint32_t lane) {

@@ -1,2 +1,7 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "run_host" 2>&1 | tail -2
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; python tools/summ.py new < gpurun_out/bench.json
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -3
+timeout 600 python tools/batch_sweep.py --shapes 4096x4096,11008x4096,4096x11008 --bits 3,4 --sparsity 0.0045 --batches 1,2 2>&1 | python3 -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print(d['shape'],d['bits'],d['batch'],d['us'],d['GBs'],d['TFLOPs'],d['speedup_vs_B_x_batch1'])
+"
