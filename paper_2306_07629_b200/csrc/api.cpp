@@ -228,32 +228,37 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
         max_nnz = std::max(max_nnz, Ls[i].max_nnz_cta);
     }
     auto al = [](size_t b, size_t a) { return (b + a - 1) / a * a; };
+    // per-layer buffers: two (layer l uses buffer l & 1, so loading layer
+    // l+1 overlaps layer l), one for a single-layer plan (more ring)
+    const size_t nbuf = n == 1 ? 1 : 2;
+    sp.nbuf = uint32_t(nbuf);
     size_t off = 1024;  // mbarriers
     sp.off_desc = uint32_t(off);
     off += 8 * 128;     // descriptor cache (stack.cu)
     sp.off_x = uint32_t(off);
     sp.nbatch = nbatch;
+    sp.nvec = nbatch;
     sp.xvec = uint32_t(al(size_t(max_ns) * kSpanCols * 2, 128) / 2);  // halves per vector
     sp.x_bytes = uint32_t(size_t(sp.xvec) * 2 * nbatch);
-    off += 2 * size_t(sp.x_bytes);
+    off += nbuf * size_t(sp.x_bytes);
     sp.off_lut = uint32_t(off);
     sp.lut_bytes = uint32_t(al(size_t(max_rows) * tile_lut_words(bits) * 4, 128));
-    off += 2 * size_t(sp.lut_bytes);
+    off += nbuf * size_t(sp.lut_bytes);
     sp.off_rp = uint32_t(off);
     sp.rp_words = uint32_t(al(max_rows + 1, 32));
-    off += 2 * size_t(sp.rp_words) * 4;
+    off += nbuf * size_t(sp.rp_words) * 4;
     sp.off_csr = uint32_t(off);
     sp.csr_cap = uint32_t(al(std::min<uint32_t>(std::max<uint32_t>(max_nnz + 4, 32), 2048), 32));
-    off += 2 * size_t(sp.csr_cap) * 4;
+    off += nbuf * size_t(sp.csr_cap) * 4;
     sp.off_hb = uint32_t(off);
     sp.hb_words = (sp.csr_cap / 32 + 16 + 3) & ~3u;  // 16-byte aligned TMA destinations
-    off += 2 * size_t(sp.hb_words) * 4;
+    off += nbuf * size_t(sp.hb_words) * 4;
     sp.off_part = uint32_t(off);
     sp.part_rows = std::max<uint32_t>(max_rows, kTileRows);
-    off = al(off + 2 * size_t(nbatch) * sp.part_rows * sp.consumers * 4, 128);
+    off = al(off + nbuf * size_t(nbatch) * sp.part_rows * sp.consumers * 4, 128);
     sp.off_seg = uint32_t(off);
     sp.seg_cap = sp.csr_cap + 128;  // one float per staged entry position (+ a round)
-    off += 2 * size_t(nbatch) * sp.seg_cap * 4;
+    off += nbuf * size_t(nbatch) * sp.seg_cap * 4;
     gseg_cap = max_nnz > sp.csr_cap - 4 ? uint32_t(al(max_nnz + 256, 4)) : 0;
     sp.off_ring = uint32_t(al(off, 1024));
     // the rest is the consumers' private rings: 2 slots per consumer warp,
@@ -307,9 +312,10 @@ struct dsq_cuda_layer {
     StackParams sp1{};                      // single-layer stack plan
     uint32_t* stack_counters = nullptr;     // [2]
     float* gseg1 = nullptr;
-    StackParams sp2{};                      // batch-2 single-layer stack plan (lazy)
-    bool sp2_ready = false;
+    StackParams sp2{}, sp4{};               // batch-2 / batch-3..4 single-layer plans (lazy)
+    bool sp2_ready = false, sp4_ready = false;
     float* gseg2 = nullptr;
+    float* gseg4 = nullptr;
     cudaStream_t stream = nullptr;
     float* batch_part = nullptr;            // batched-product slice partials (lazy)
     uint32_t batch_kslices = 0, batch_spans = 0;
@@ -708,6 +714,7 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (L->dense_w) cudaFree(L->dense_w);
     if (L->batch_part) cudaFree(L->batch_part);
     if (L->gseg2) cudaFree(L->gseg2);
+    if (L->gseg4) cudaFree(L->gseg4);
     if (L->arena) cudaFree(L->arena);
     delete L;
     return DSQ_OK;
@@ -779,22 +786,28 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
     auto* L = const_cast<dsq_cuda_layer*>(Lc);
     if (!L || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     if (batch < 1 || batch > 16) return fail(DSQ_E_INVALID_ARGUMENT, "batch must be 1..16");
-    if (batch == 2 && L->rec_layout && (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
+    if (batch >= 2 && batch <= 4 && L->rec_layout &&
+        (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
         x_dtype == DSQ_F16 && (y_dtype == DSQ_F32 || y_dtype == DSQ_F16) &&
         !(reinterpret_cast<uintptr_t>(x) & 15u) && L->cols % 8 == 0) {
-        // K7 with two activation vectors in one launch: both share every
-        // decoded weight fragment (the free HMMA B columns 4..7)
+        // K7 with 2 or 4 activation vectors in one launch: all share every
+        // decoded weight fragment (vectors 0/1 in the HMMA B columns 0..3 /
+        // 4..7, vectors 2/3 in a second HMMA on the same A fragment)
+        const uint32_t nb = batch == 2 ? 2u : 4u;
+        StackParams& spb = nb == 2 ? L->sp2 : L->sp4;
         {
             std::lock_guard<std::mutex> lk(L->mu);
-            if (!L->sp2_ready) {
+            bool& ready = nb == 2 ? L->sp2_ready : L->sp4_ready;
+            float*& gbuf = nb == 2 ? L->gseg2 : L->gseg4;
+            if (!ready) {
                 uint32_t gcap = 0;
                 StackPlanLayer pl{L->rows, L->cols, L->tiles, L->ns,
                                   max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
-                int prc = plan_stack(&pl, 1, L->num_sms, L->bits, L->sp2, gcap, 2);
+                int prc = plan_stack(&pl, 1, L->num_sms, L->bits, spb, gcap, nb);
                 if (prc) return prc;
                 if (gcap)
-                    CUDA_TRY(cudaMalloc(&L->gseg2, size_t(L->num_sms) * 2 * 2 * gcap * 4 + 4));
-                StackParams& q = L->sp2;
+                    CUDA_TRY(cudaMalloc(&gbuf, size_t(L->num_sms) * 2 * nb * gcap * 4 + 4));
+                StackParams& q = spb;
                 const StackLayerDesc& d1 = L->sp1.inl[0];
                 StackLayerDesc& d = q.inl[0];
                 d.idx = d1.idx;
@@ -806,12 +819,13 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
                 d.dep = kNoDep;
                 d.reduce_ord = kNoDep;
                 q.counters = L->sp1.counters;
-                q.gseg = L->gseg2;
+                q.gseg = gbuf;
                 q.gseg_cap = gcap;
-                L->sp2_ready = true;
+                ready = true;
             }
         }
-        StackParams sp = L->sp2;
+        StackParams sp = spb;
+        sp.nvec = batch;
         StackLayerDesc& d = sp.inl[0];
         d.x = static_cast<const uint16_t*>(x);
         d.y = y;

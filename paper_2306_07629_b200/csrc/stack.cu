@@ -229,7 +229,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     // the partial tables start at zero; the finisher re-zeroes what it reads
     {
         float* part = reinterpret_cast<float*>(sm + p.off_part);
-        for (uint32_t i = threadIdx.x; i < 2 * NB * NC * p.part_rows; i += blockDim.x) part[i] = 0.f;
+        for (uint32_t i = threadIdx.x; i < p.nbuf * NB * NC * p.part_rows; i += blockDim.x) part[i] = 0.f;
     }
     __syncthreads();
 
@@ -291,8 +291,13 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             // zero padding to the span count), completion on xfull[b]
             auto stage_x = [&]() {
                 const uint32_t body = (d.cols / 8) * 16;  // bytes
+                const uint32_t nv = NB == 1 ? 1u : p.nvec;
+                // vectors past nvec are not staged: their B columns and
+                // accumulators are separate from the real vectors' and their
+                // results are never stored, so stale data there is harmless
 #pragma unroll
                 for (int v = 0; v < NB; ++v) {  // batch vector v at xb + v * xvec halves
+                    if (uint32_t(v) >= nv) continue;
                     uint16_t* xv = reinterpret_cast<uint16_t*>(xb) + v * p.xvec;
                     const uint16_t* gx = d.x + size_t(v) * p.x_bstride;
                     for (uint32_t i = body / 2 + lane; i < d.ns * kSpanCols; i += 32)
@@ -301,12 +306,13 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 __syncwarp();
                 if (lane == 0) {
                     fence_proxy_async_global();
-                    mbar_arrive_expect_tx(&xfull[b], NB * body);
+                    mbar_arrive_expect_tx(&xfull[b], nv * body);
                     if (body)
 #pragma unroll
                         for (int v = 0; v < NB; ++v)
-                            bulk_g2s_plain(reinterpret_cast<uint16_t*>(xb) + v * p.xvec,
-                                           d.x + size_t(v) * p.x_bstride, body, &xfull[b]);
+                            if (uint32_t(v) < nv)
+                                bulk_g2s_plain(reinterpret_cast<uint16_t*>(xb) + v * p.xvec,
+                                               d.x + size_t(v) * p.x_bstride, body, &xfull[b]);
                 }
             };
             if (d.dep == kNoDep) stage_x();  // external input: no wait at all
@@ -383,26 +389,33 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 s += part[w * p.part_rows + i];
                 part[w * p.part_rows + i] = 0.f;
             }
-            float s1 = 0.f;  // batch vector 1 (NB == 2)
-            if constexpr (NB == 2) {
-                float* part1 = part + NC * p.part_rows;
+            float sv[NB > 1 ? NB - 1 : 1];  // batch vectors 1.. (NB > 1)
+#pragma unroll
+            for (int v = 1; v < NB; ++v) {
+                float* pv = part + v * NC * p.part_rows;
+                float t = 0.f;
 #pragma unroll
                 for (uint32_t w = 0; w < NC; ++w) {
-                    s1 += part1[w * p.part_rows + i];
-                    part1[w * p.part_rows + i] = 0.f;
+                    t += pv[w * p.part_rows + i];
+                    pv[w * p.part_rows + i] = 0.f;
                 }
+                sv[v - 1] = t;
             }
             if (i >= nrows) continue;  // padding rows of the last tile
             const uint32_t a = rp[i] - ea, e = rp[i + 1] - ea;
             for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j) {
-                s += S[j * 128 + min(e - 1 - j * 128, 127u)];
-                if constexpr (NB == 2) s1 += S[s_vec + j * 128 + min(e - 1 - j * 128, 127u)];
+                const uint32_t q = j * 128 + min(e - 1 - j * 128, 127u);
+                s += S[q];
+#pragma unroll
+                for (int v = 1; v < NB; ++v) sv[v - 1] += S[v * s_vec + q];
             }
-            if constexpr (NB == 2) {
+#pragma unroll
+            for (int v = 1; v < NB; ++v) {
+                if (uint32_t(v) >= p.nvec) continue;
                 if (d.y_f16)
-                    static_cast<__half*>(d.y)[p.y_bstride + r0 + i] = __float2half_rn(s1);
+                    static_cast<__half*>(d.y)[v * p.y_bstride + r0 + i] = __float2half_rn(sv[v - 1]);
                 else
-                    static_cast<float*>(d.y)[p.y_bstride + r0 + i] = s1;
+                    static_cast<float*>(d.y)[v * p.y_bstride + r0 + i] = sv[v - 1];
             }
             if (tp) {
                 // a partial sum: hand it to every rank (own included) at slot
@@ -517,8 +530,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             if (e1 > e0) {
 #pragma unroll
                 for (int v = 0; v < NB; ++v)
-                    csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh + v * p.xvec,
-                               S + v * (staged ? p.seg_cap : p.gseg_cap), cw, kCsrWarps, lane);
+                    if (v == 0 || uint32_t(v) < p.nvec)
+                        csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh + v * p.xvec,
+                                   S + v * (staged ? p.seg_cap : p.gseg_cap), cw, kCsrWarps, lane);
             }
             __syncwarp();
             if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrDone);
@@ -536,7 +550,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     const uint32_t cw = warp;
     // this lane's B-column x halves (NB == 2: B columns 4..7, lanes 16..31,
     // read batch vector 1)
-    const uint32_t xoff = tile_x_offset(lane) + (NB == 2 ? (lane >> 4) * p.xvec : 0u);
+    const uint32_t xoff = tile_x_offset(lane) + (NB >= 2 ? (lane >> 4) * p.xvec : 0u);
     const uint32_t trow = (lane >> 2) & 3u;         // tile row of this lane
     const uint64_t policy = policy_evict_first();
     // this warp's weight stream: its unit range of every layer, in chunks of
@@ -624,6 +638,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         uint32_t cur_tile = 0xffffffffu;
         Planes16 P;
         float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+        float e0[4] = {0.f, 0.f, 0.f, 0.f}, e1[4] = {0.f, 0.f, 0.f, 0.f};  // vectors 2/3 (NB == 4)
         auto flush = [&]() {
             if (cur_tile != 0xffffffffu) {
                 if constexpr (NB == 1) {
@@ -634,6 +649,14 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                     if ((lane & 1) == 0 && lane < 16)
                         part[((lane >> 1) & 1u) * NC * p.part_rows + cw * p.part_rows +
                              cur_tile * kTileRows + trow] += v;
+                    if constexpr (NB == 4) {  // vectors 2/3 from the second accumulators
+                        const float v2 = tile_rows_reduce2(e0, e1, lane);
+                        if ((lane & 1) == 0 && lane < 16)
+                            part[(2u + ((lane >> 1) & 1u)) * NC * p.part_rows + cw * p.part_rows +
+                                 cur_tile * kTileRows + trow] += v2;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) e0[k] = e1[k] = 0.f;
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) d0[k] = d1[k] = 0.f;
@@ -684,7 +707,26 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         xb2 = *reinterpret_cast<const uint4*>(xsp + 128);
                     };
                     uint32_t k = s;
-                    if constexpr (BITS == 3) {
+                    if constexpr (NB == 4) {
+                        // four vectors: every decoded fragment feeds two HMMAs
+                        // (vectors 0/1 and 2/3, x at +2 vector strides)
+                        for (; k < s_end; ++k) {
+                            const uint4 xa0 = *reinterpret_cast<const uint4*>(xs);
+                            const uint4 xb0 = *reinterpret_cast<const uint4*>(xs + 128);
+                            const uint4 ya0 = *reinterpret_cast<const uint4*>(xs + 2 * p.xvec);
+                            const uint4 yb0 = *reinterpret_cast<const uint4*>(xs + 2 * p.xvec + 128);
+                            if constexpr (BITS == 3) {
+                                span3_mma_x2(sp[lane], sp[32 + lane], sp[64 + lane], P.a, xa0, xb0,
+                                             ya0, yb0, d0, d1, e0, e1);
+                            } else {
+                                span4_mma_x2(reinterpret_cast<const uint4*>(sp)[lane], P, xa0, xb0,
+                                             ya0, yb0, d0, d1, e0, e1);
+                            }
+                            sp += UW;
+                            xs += kSpanCols;
+                        }
+                    }
+                    if constexpr (BITS == 3 && NB != 4) {
                         // span pairs: two independent units per iteration
                         for (; k + 1 < s_end; k += 2) {
                             const uint32_t a0 = sp[lane], a1 = sp[32 + lane], a2 = sp[64 + lane];
@@ -765,15 +807,16 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static bool attr_done[8][64] = {};
+    static bool attr_done[12][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     const int ci = p.consumers == 8 ? 0 : 1;
-    const int bi = (p.nbatch == 2 ? 4 : 0) + (p.bits == 3 ? 0 : 1) * 2 + ci;
+    const int bi = (p.nbatch == 4 ? 8 : p.nbatch == 2 ? 4 : 0) + (p.bits == 3 ? 0 : 1) * 2 + ci;
     using K = void (*)(StackParams);
-    static const K kerns[8] = {stack_gemv<3, 8, 1>,  stack_gemv<3, 16, 1>, stack_gemv<4, 8, 1>,
-                               stack_gemv<4, 16, 1>, stack_gemv<3, 8, 2>,  stack_gemv<3, 16, 2>,
-                               stack_gemv<4, 8, 2>,  stack_gemv<4, 16, 2>};
+    static const K kerns[12] = {
+        stack_gemv<3, 8, 1>, stack_gemv<3, 16, 1>, stack_gemv<4, 8, 1>, stack_gemv<4, 16, 1>,
+        stack_gemv<3, 8, 2>, stack_gemv<3, 16, 2>, stack_gemv<4, 8, 2>, stack_gemv<4, 16, 2>,
+        stack_gemv<3, 8, 4>, stack_gemv<3, 16, 4>, stack_gemv<4, 8, 4>, stack_gemv<4, 16, 4>};
     const K kern = kerns[bi];
     if (dev < 0 || dev >= 64 || !attr_done[bi][dev]) {
         int max_optin = 0;

@@ -100,7 +100,9 @@ struct StackParams {
     // decoded A fragment -- vector b feeds the HMMA B columns 4b..4b+3, which
     // the block-diagonal map leaves free at batch 1.  x buffers, partial
     // tables and CSR scan buffers hold nbatch vectors each.
-    uint32_t nbatch;                 // 1 or 2
+    uint32_t nbatch;                 // 1, 2 or 4 (vectors 2/3: a second HMMA per fragment)
+    uint32_t nvec;                   // vectors actually supplied (<= nbatch; the rest are 0)
+    uint32_t nbuf;                   // per-layer buffers (2; 1 for single-layer plans)
     uint32_t xvec;                   // halves between the vectors in an smem x buffer
     uint32_t x_bstride, y_bstride;   // elements between the vectors in global x / y
     // tensor parallelism (world > 1): the partial y of a reduce layer is
