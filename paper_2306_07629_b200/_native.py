@@ -157,6 +157,10 @@ PROTOTYPES = {
     "dsq_cuda_container_layer": (C.c_void_p, [C.c_void_p, C.c_uint32]),
     "dsq_cuda_container_layer_name": (C.c_char_p, [C.c_void_p, C.c_uint32]),
     "dsq_cuda_container_close": (C.c_int, [C.c_void_p]),
+    "dsq_cuda_stack_create_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32,
+                                              C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                                              C.POINTER(C.c_void_p), C.c_int, C.c_uint32,
+                                              C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
     "dsq_cuda_stack_run_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                           C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "dsq_decode_step_costs": (C.c_int, [C.POINTER(ModelShape), C.POINTER(HwProfile),

@@ -987,10 +987,26 @@ struct dsq_cuda_stack {
 static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
                              const void* const* xs, void* const* ys, int y_dtype,
                              const uint8_t* reduce, dsq_cuda_tp* tp, uint32_t grid,
-                             dsq_cuda_stack** out) {
+                             dsq_cuda_stack** out, uint32_t batch = 1, uint32_t x_bstride = 0,
+                             uint32_t y_bstride = 0) {
     if (!out || !layers || !deps || !xs || !ys || n == 0)
         return fail(DSQ_E_INVALID_ARGUMENT, "stack: null argument or empty stack");
     *out = nullptr;
+    if (batch < 1 || batch > 4)
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack: batch must be 1..4");
+    const uint32_t nbatch = batch == 1 ? 1u : batch == 2 ? 2u : 4u;
+    if (batch > 1) {
+        if (tp) return fail(DSQ_E_UNSUPPORTED, "stack: batched stacks are single-GPU");
+        if (x_bstride % 8 || y_bstride % 8)
+            return fail(DSQ_E_INVALID_ARGUMENT, "stack: batch strides must be multiples of 8");
+        for (uint32_t i = 0; i < n; ++i) {
+            if (!layers[i]) break;
+            if (layers[i]->rows > y_bstride)
+                return fail(DSQ_E_INVALID_ARGUMENT, "stack: y batch stride < rows of layer %u", i);
+            if (deps[i] < 0 && layers[i]->cols > x_bstride)
+                return fail(DSQ_E_INVALID_ARGUMENT, "stack: x batch stride < cols of layer %u", i);
+        }
+    }
     if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
         return fail(DSQ_E_INVALID_ARGUMENT, "stack: y dtype must be F32 or F16");
     const dsq_cuda_layer* L0 = layers[0];
@@ -1036,7 +1052,7 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     S->n_reduce = n_reduce;
     S->tp = tp;
     uint32_t gseg_cap = 0;
-    int rc = plan_stack(pl.data(), n, G, L0->bits, S->sp, gseg_cap);
+    int rc = plan_stack(pl.data(), n, G, L0->bits, S->sp, gseg_cap, nbatch);
     if (rc) {
         delete S;
         return rc;
@@ -1057,7 +1073,7 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     const size_t tb = (size_t(n) * sizeof(StackLayerDesc) + 255) & ~size_t(255);
     const size_t cb = ((size_t(n) + 1) * 4 + 255) & ~size_t(255);
     const size_t rb = (rng.size() * 4 + 255) & ~size_t(255);
-    const size_t gb = size_t(G) * 2 * gseg_cap * 4 + 4;
+    const size_t gb = size_t(G) * 2 * nbatch * gseg_cap * 4 + 4;
     cudaError_t e = cudaMalloc(&S->arena, tb + cb + rb + gb);
     if (e != cudaSuccess) {
         delete S;
@@ -1098,6 +1114,9 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     S->sp.counters = reinterpret_cast<uint32_t*>(base + tb);
     S->sp.gseg = reinterpret_cast<float*>(base + tb + cb + rb);
     S->sp.gseg_cap = gseg_cap;
+    S->sp.nvec = batch;
+    S->sp.x_bstride = x_bstride;
+    S->sp.y_bstride = y_bstride;
     S->sp.n_layers = n;
     S->sp.tp_world = tp ? tp->world : 1;
     S->sp.tp_rank = tp ? tp->rank : 0;
@@ -1136,6 +1155,14 @@ int dsq_cuda_stack_create_tp(dsq_cuda_layer* const* layers, uint32_t n, const in
                              const uint8_t* reduce, dsq_cuda_tp* tp, uint32_t grid,
                              dsq_cuda_stack** out) {
     return stack_create_impl(layers, n, deps, xs, ys, y_dtype, reduce, tp, grid, out);
+}
+
+int dsq_cuda_stack_create_batch(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                                const void* const* xs, void* const* ys, int y_dtype,
+                                uint32_t batch, uint32_t x_bstride, uint32_t y_bstride,
+                                dsq_cuda_stack** out) {
+    return stack_create_impl(layers, n, deps, xs, ys, y_dtype, nullptr, nullptr, 0, out, batch,
+                             x_bstride, y_bstride);
 }
 
 // ---- tensor-parallel context: this rank's receive buffer + flags, peers mapped

@@ -292,6 +292,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             auto stage_x = [&]() {
                 const uint32_t body = (d.cols / 8) * 16;  // bytes
                 const uint32_t nv = NB == 1 ? 1u : p.nvec;
+                // a chained layer's x vectors are its producer's y vectors
+                const uint32_t xstride = d.dep == kNoDep ? p.x_bstride : p.y_bstride;
                 // vectors past nvec are not staged: their B columns and
                 // accumulators are separate from the real vectors' and their
                 // results are never stored, so stale data there is harmless
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 for (int v = 0; v < NB; ++v) {  // batch vector v at xb + v * xvec halves
                     if (uint32_t(v) >= nv) continue;
                     uint16_t* xv = reinterpret_cast<uint16_t*>(xb) + v * p.xvec;
-                    const uint16_t* gx = d.x + size_t(v) * p.x_bstride;
+                    const uint16_t* gx = d.x + size_t(v) * xstride;
                     for (uint32_t i = body / 2 + lane; i < d.ns * kSpanCols; i += 32)
                         xv[i] = i < d.cols ? ld_cg_u16(gx + i) : uint16_t(0);
                 }
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         for (int v = 0; v < NB; ++v)
                             if (uint32_t(v) < nv)
                                 bulk_g2s_plain(reinterpret_cast<uint16_t*>(xb) + v * p.xvec,
-                                               d.x + size_t(v) * p.x_bstride, body, &xfull[b]);
+                                               d.x + size_t(v) * xstride, body, &xfull[b]);
                 }
             };
             if (d.dep == kNoDep) stage_x();  // external input: no wait at all

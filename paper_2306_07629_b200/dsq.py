@@ -252,10 +252,13 @@ class DeviceStack:
     is layer i's x, or -1 for the external fp16 buffer xs[i] (device pointer).
     With ``tp`` (a TPContext), layers with reduce[i] produce partial sums that
     the kernel all-reduces over the ranks' peer memory (dsq_cuda_stack_create_tp);
-    ``grid`` = CTAs (0: one per SM)."""
+    ``grid`` = CTAs (0: one per SM).  ``batch`` (1..4) activation vectors at
+    once: vector v of an external x at xs[i] + v * x_stride halves, of every
+    output at ys[i] + v * y_stride elements (dsq_cuda_stack_create_batch)."""
 
     def __init__(self, layers: list, deps: list, xs: list, ys: list, y_dtype: int,
-                 reduce: list | None = None, tp: "TPContext | None" = None, grid: int = 0):
+                 reduce: list | None = None, tp: "TPContext | None" = None, grid: int = 0,
+                 batch: int = 1, x_stride: int = 0, y_stride: int = 0):
         n = len(layers)
         self._layers = list(layers)  # keep the layer handles alive
         self._tp = tp
@@ -264,7 +267,12 @@ class DeviceStack:
         arr_x = (C.c_void_p * n)(*[x or 0 for x in xs])
         arr_y = (C.c_void_p * n)(*ys)
         h = C.c_void_p()
-        if tp is None and reduce is None and grid == 0:
+        if batch > 1:
+            if tp is not None or reduce is not None:
+                raise DsqError(102, "batched stacks are single-GPU")
+            check(lib.dsq_cuda_stack_create_batch(arr_l, n, arr_d, arr_x, arr_y, y_dtype, batch,
+                                                  x_stride, y_stride, C.byref(h)))
+        elif tp is None and reduce is None and grid == 0:
             check(lib.dsq_cuda_stack_create(arr_l, n, arr_d, arr_x, arr_y, y_dtype, C.byref(h)))
         else:
             red = (C.c_uint8 * n)(*([1 if r else 0 for r in reduce] if reduce else [0] * n))

@@ -17,7 +17,7 @@ tensor-parallel (configs[3]): v,q,k,up,gate column-parallel, o,down
 row-parallel, the two all-reduces per decoder layer fused into the stack
 kernel over NVLink peer memory; timing is the max over ranks.
 
-usage: python tools/bench_stack.py [--model 13b] [--tokens 3] [--rotation 8]
+usage: python tools/bench_stack.py [--model 13b] [--tokens 3] [--rotation 8] [--batch 1..4]
        torchrun --nproc-per-node 8 tools/bench_stack.py --model 65b
 """
 import argparse
@@ -68,7 +68,7 @@ def fast_layer(rows, cols, bits=3, sparsity=0.0045, seed=0):
     return QuantizedLayer(f"{rows}x{cols}", rows, cols, packed, sparse, 10), int(pos.size)
 
 
-def run(model, tokens, rotation, peak, rank=0, world=1):
+def run(model, tokens, rotation, peak, rank=0, world=1, batch=1):
     import torch
     import paper_2306_07629_b200._native as N
     from paper_2306_07629_b200 import DeviceLayer, DeviceStack
@@ -90,8 +90,11 @@ def run(model, tokens, rotation, peak, rank=0, world=1):
     shards = shard_decoder(qls, rank, world) if world > 1 else qls
     dev = torch.cuda.current_device()
     dls = [[DeviceLayer(q, device=dev) for q in shards] for _ in range(rotation)]
-    x = torch.from_numpy(make_x(h).view(np.int16)).cuda()
-    ys = [[torch.empty(q.rows, dtype=torch.int16, device="cuda") for q in shards]
+    # batch B: B sequences decoded together, vector v at +v * stride
+    YS = max(h, f)
+    x = torch.from_numpy(np.tile(make_x(h), batch).view(np.int16)).cuda()
+    ys = [[torch.empty(q.rows * batch if batch == 1 else YS * batch, dtype=torch.int16,
+                       device="cuda") for q in shards]
           for _ in range(rotation)]
     tp = None
     if world > 1:
@@ -112,6 +115,8 @@ def run(model, tokens, rotation, peak, rank=0, world=1):
             layers += dls[slot]
             yp += [y.data_ptr() for y in ys[slot]]
         xp = [x.data_ptr() if d < 0 else 0 for d in deps]
+        if batch > 1:
+            return DeviceStack(layers, deps, xp, yp, N.F16, batch=batch, x_stride=h, y_stride=YS)
         if tp is None:
             return DeviceStack(layers, deps, xp, yp, N.F16)
         return DeviceStack(layers, deps, xp, yp, N.F16, reduce=reduce, tp=tp)
@@ -137,10 +142,10 @@ def run(model, tokens, rotation, peak, rank=0, world=1):
     gbs = bytes_dec * nl * tokens / (ms * 1e-3) / 1e9
     return {
         "model": f"llama-{model} linear stack ({nl} decoder layers x 7 GEMVs, 3-bit + 0.45% CSR)",
-        "tokens": tokens, "gpus": world, "parallelism": f"tp{world}",
+        "tokens": tokens, "gpus": world, "parallelism": f"tp{world}", "batch": batch,
         "us_per_gemv": round(ms * 1e3 / gemvs, 3),
         "ms_per_token": round(ms / tokens, 4),
-        "decode_tok_s_linear": round(tokens / (ms * 1e-3), 1),
+        "decode_tok_s_linear": round(batch * tokens / (ms * 1e-3), 1),
         "effective_GBs": round(gbs, 1), "frac_of_peak_per_gpu": round(gbs / world / peak, 4),
         "bytes_per_token": bytes_dec * nl, "rotation": rotation, "setup_s": round(setup, 1),
     }
@@ -151,6 +156,7 @@ def main():
     ap.add_argument("--model", default="13b", choices=list(MODELS) + ["all"])
     ap.add_argument("--tokens", type=int, default=3)
     ap.add_argument("--rotation", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1..4)")
     args = ap.parse_args()
     try:
         peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
@@ -165,7 +171,7 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     for m in (list(MODELS) if args.model == "all" else [args.model]):
-        line = run(m, args.tokens, args.rotation, peak, rank, world)
+        line = run(m, args.tokens, args.rotation, peak, rank, world, args.batch)
         if rank == 0:
             print(json.dumps(line), flush=True)
     if world > 1:
