@@ -212,7 +212,7 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, 
 }
 
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
-               uint32_t& gseg_cap, uint32_t nbatch = 1) {
+               uint32_t& gseg_cap, uint32_t nbatch = 1, bool x_shared = false) {
     int dev = 0, smax = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -240,7 +240,9 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.nvec = nbatch;
     sp.xvec = uint32_t(al(size_t(max_ns) * kSpanCols * 2, 128) / 2);  // halves per vector
     sp.x_bytes = uint32_t(size_t(sp.xvec) * 2 * nbatch);
-    off += nbuf * size_t(sp.x_bytes);
+    const size_t nbuf_x = x_shared ? 1 : nbuf;
+    sp.x_step = nbuf_x == 2 ? sp.x_bytes : 0u;
+    off += nbuf_x * size_t(sp.x_bytes);
     sp.off_lut = uint32_t(off);
     sp.lut_bytes = uint32_t(al(size_t(max_rows) * tile_lut_words(bits) * 4, 128));
     off += nbuf * size_t(sp.lut_bytes);
@@ -267,9 +269,13 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     const size_t ring = size_t(smax) > sp.off_ring ? size_t(smax) - sp.off_ring : 0;
     sp.n_slots = sp.consumers * 2;
     sp.slot_bytes = uint32_t(ring / sp.n_slots / ub * ub);
-    if (sp.slot_bytes < 2 * ub)
+    if (sp.slot_bytes < 2 * ub) {
+        // large batched x: retry with one shared x buffer before giving up
+        if (nbatch > 1 && nbuf == 2 && !x_shared)
+            return plan_stack(Ls, n, G, bits, sp, gseg_cap, nbatch, true);
         return fail(DSQ_E_UNSUPPORTED, "stack: layer too large for the shared-memory ring "
                     "(x %u B)", sp.x_bytes);
+    }
     sp.smem_bytes = sp.off_ring + sp.n_slots * sp.slot_bytes;
     sp.grid = uint32_t(G);
     sp.bits = bits;

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             const StackLayerDesc& d = sd.d;
             const Share sh = cta_share(d, cta);
             const uint32_t r0 = sh.r0, r1 = sh.r0 + sh.nrows;
-            uint8_t* xb = sm + p.off_x + b * p.x_bytes;
+            uint8_t* xb = sm + p.off_x + b * p.x_step;
             if (lane == 0) {
                 DSQ_TRACE(l, kTrLoaderStart);
                 // the CTA's LUT planes ride on the x barrier (expected first,
@@ -317,6 +317,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                                                d.x + size_t(v) * xstride, body, &xfull[b]);
                 }
             };
+            // one shared x buffer (large batched stacks, p.x_step == 0): layer
+            // l may overwrite x only after every reader of layer l-1's x is done
+            if (p.x_step == 0 && l >= 1) mbar_wait(&bempty[(l - 1) & 1u], ((l - 1) >> 1) & 1u);
             if (d.dep == kNoDep) stage_x();  // external input: no wait at all
             // row_ptr slice + CSR entries + row-start bitmap of the CTA's rows:
             // TMA bulk copies (16-byte granules; the device arrays are padded),
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             mbar_wait(&cfull[b], ph);
             if (l >= 2) mbar_wait(&pempty[b], ((l >> 1) - 1) & 1u);  // segs consumed
             if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrStaged);
-            const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_bytes);
+            const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);
             const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
             (void)rp;
             const uint32_t e0 = sd.e0, e1 = sd.e1, ea = e0 & ~3u;
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         if (l >= 2) mbar_wait(&pempty[b], ((l >> 1) - 1) & 1u);
         DSQ_LAP(c_xw);
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrXReady);
-        const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_bytes);
+        const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);
         const uint32_t* luts = reinterpret_cast<const uint32_t*>(sm + p.off_lut + b * p.lut_bytes);
         float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * NB * p.part_rows * NC;
 

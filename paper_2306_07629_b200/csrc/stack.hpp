@@ -89,6 +89,7 @@ struct StackParams {
     uint32_t off_desc;               // 8 x 128-byte layer descriptor cache
     uint32_t off_ring, slot_bytes, n_slots;
     uint32_t off_x, x_bytes;         // two x buffers
+    uint32_t x_step;                 // bytes between them (0: one shared x buffer)
     uint32_t off_lut, lut_bytes;     // two LUT-plane buffers (the CTA's tiles)
     uint32_t off_rp, rp_words;       // two row_ptr slices
     uint32_t off_csr, csr_cap;       // two CSR entry buffers (entries)
