@@ -221,6 +221,7 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
         const int c = atoi(e);
         if (c == 8 || c == 16) sp.consumers = uint32_t(c);
     }
+    if (nbatch == 8) sp.consumers = 8;  // four accumulator pairs: 8-consumer kernels only
     uint32_t max_ns = 0, max_rows = 0, max_nnz = 0;
     for (uint32_t i = 0; i < n; ++i) {
         max_ns = std::max(max_ns, Ls[i].ns);
@@ -318,10 +319,11 @@ struct dsq_cuda_layer {
     StackParams sp1{};                      // single-layer stack plan
     uint32_t* stack_counters = nullptr;     // [2]
     float* gseg1 = nullptr;
-    StackParams sp2{}, sp4{};               // batch-2 / batch-3..4 single-layer plans (lazy)
-    bool sp2_ready = false, sp4_ready = false;
+    StackParams sp2{}, sp4{}, sp8{};        // batch 2 / 3..4 / 5..8 single-layer plans (lazy)
+    bool sp2_ready = false, sp4_ready = false, sp8_ready = false, sp8_failed = false;
     float* gseg2 = nullptr;
     float* gseg4 = nullptr;
+    float* gseg8 = nullptr;
     cudaStream_t stream = nullptr;
     float* batch_part = nullptr;            // batched-product slice partials (lazy)
     uint32_t batch_kslices = 0, batch_spans = 0;
@@ -721,6 +723,7 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (L->batch_part) cudaFree(L->batch_part);
     if (L->gseg2) cudaFree(L->gseg2);
     if (L->gseg4) cudaFree(L->gseg4);
+    if (L->gseg8) cudaFree(L->gseg8);
     if (L->arena) cudaFree(L->arena);
     delete L;
     return DSQ_OK;
@@ -792,24 +795,29 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
     auto* L = const_cast<dsq_cuda_layer*>(Lc);
     if (!L || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     if (batch < 1 || batch > 16) return fail(DSQ_E_INVALID_ARGUMENT, "batch must be 1..16");
-    if (batch >= 2 && batch <= 4 && L->rec_layout &&
+    const uint32_t nbk = batch == 2 ? 2u : batch <= 4 ? 4u : 8u;
+    if (batch >= 2 && batch <= 8 && L->rec_layout && !(nbk == 8 && L->sp8_failed) &&
         (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
         x_dtype == DSQ_F16 && (y_dtype == DSQ_F32 || y_dtype == DSQ_F16) &&
         !(reinterpret_cast<uintptr_t>(x) & 15u) && L->cols % 8 == 0) {
         // K7 with 2 or 4 activation vectors in one launch: all share every
         // decoded weight fragment (vectors 0/1 in the HMMA B columns 0..3 /
         // 4..7, vectors 2/3 in a second HMMA on the same A fragment)
-        const uint32_t nb = batch == 2 ? 2u : 4u;
-        StackParams& spb = nb == 2 ? L->sp2 : L->sp4;
+        const uint32_t nb = nbk;
+        StackParams& spb = nb == 2 ? L->sp2 : nb == 4 ? L->sp4 : L->sp8;
         {
             std::lock_guard<std::mutex> lk(L->mu);
-            bool& ready = nb == 2 ? L->sp2_ready : L->sp4_ready;
-            float*& gbuf = nb == 2 ? L->gseg2 : L->gseg4;
+            bool& ready = nb == 2 ? L->sp2_ready : nb == 4 ? L->sp4_ready : L->sp8_ready;
+            float*& gbuf = nb == 2 ? L->gseg2 : nb == 4 ? L->gseg4 : L->gseg8;
             if (!ready) {
                 uint32_t gcap = 0;
                 StackPlanLayer pl{L->rows, L->cols, L->tiles, L->ns,
                                   max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
                 int prc = plan_stack(&pl, 1, L->num_sms, L->bits, spb, gcap, nb);
+                if (prc && nb == 8) {  // 8 x vectors do not fit: the K8 path
+                    L->sp8_failed = true;
+                    goto batched_k8;
+                }
                 if (prc) return prc;
                 if (gcap)
                     CUDA_TRY(cudaMalloc(&gbuf, size_t(L->num_sms) * 2 * nb * gcap * 4 + 4));
@@ -847,6 +855,7 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
         CUDA_TRY(launch_stack(sp, st, pdl));
         return DSQ_OK;
     }
+batched_k8:
     if (batch > 1) return gemv_batch(L, kernel, x, x_dtype, y, y_dtype, batch, st);
     if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)
         return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);

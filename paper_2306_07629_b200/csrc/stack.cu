@@ -643,7 +643,13 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         uint32_t cur_tile = 0xffffffffu;
         Planes16 P;
         float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-        float e0[4] = {0.f, 0.f, 0.f, 0.f}, e1[4] = {0.f, 0.f, 0.f, 0.f};  // vectors 2/3 (NB == 4)
+        // vector pairs 2/3, 4/5, 6/7 (NB >= 4): one accumulator pair each
+        constexpr int NX = NB >= 4 ? NB / 2 - 1 : 1;
+        float ex[NX][2][4];
+#pragma unroll
+        for (int q = 0; q < NX; ++q)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ex[q][0][k] = ex[q][1][k] = 0.f;
         auto flush = [&]() {
             if (cur_tile != 0xffffffffu) {
                 if constexpr (NB == 1) {
@@ -654,13 +660,16 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                     if ((lane & 1) == 0 && lane < 16)
                         part[((lane >> 1) & 1u) * NC * p.part_rows + cw * p.part_rows +
                              cur_tile * kTileRows + trow] += v;
-                    if constexpr (NB == 4) {  // vectors 2/3 from the second accumulators
-                        const float v2 = tile_rows_reduce2(e0, e1, lane);
-                        if ((lane & 1) == 0 && lane < 16)
-                            part[(2u + ((lane >> 1) & 1u)) * NC * p.part_rows + cw * p.part_rows +
-                                 cur_tile * kTileRows + trow] += v2;
+                    if constexpr (NB >= 4) {  // the other vector pairs
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) e0[k] = e1[k] = 0.f;
+                        for (int q = 0; q < NX; ++q) {
+                            const float v2 = tile_rows_reduce2(ex[q][0], ex[q][1], lane);
+                            if ((lane & 1) == 0 && lane < 16)
+                                part[(2u * (q + 1) + ((lane >> 1) & 1u)) * NC * p.part_rows +
+                                     cw * p.part_rows + cur_tile * kTileRows + trow] += v2;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) ex[q][0][k] = ex[q][1][k] = 0.f;
+                        }
                     }
                 }
 #pragma unroll
@@ -712,26 +721,30 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         xb2 = *reinterpret_cast<const uint4*>(xsp + 128);
                     };
                     uint32_t k = s;
-                    if constexpr (NB == 4) {
-                        // four vectors: every decoded fragment feeds two HMMAs
-                        // (vectors 0/1 and 2/3, x at +2 vector strides)
+                    if constexpr (NB >= 4) {
+                        // 4 / 8 vectors: every decoded fragment feeds NB/2
+                        // HMMAs (vector pair q's x at +2q vector strides)
                         for (; k < s_end; ++k) {
                             const uint4 xa0 = *reinterpret_cast<const uint4*>(xs);
                             const uint4 xb0 = *reinterpret_cast<const uint4*>(xs + 128);
-                            const uint4 ya0 = *reinterpret_cast<const uint4*>(xs + 2 * p.xvec);
-                            const uint4 yb0 = *reinterpret_cast<const uint4*>(xs + 2 * p.xvec + 128);
+                            uint4 ya[NX], yb[NX];
+#pragma unroll
+                            for (int q = 0; q < NX; ++q) {
+                                ya[q] = *reinterpret_cast<const uint4*>(xs + 2 * (q + 1) * p.xvec);
+                                yb[q] = *reinterpret_cast<const uint4*>(xs + 2 * (q + 1) * p.xvec + 128);
+                            }
                             if constexpr (BITS == 3) {
-                                span3_mma_x2(sp[lane], sp[32 + lane], sp[64 + lane], P.a, xa0, xb0,
-                                             ya0, yb0, d0, d1, e0, e1);
+                                span3_mma_xn<NX>(sp[lane], sp[32 + lane], sp[64 + lane], P.a, xa0,
+                                                 xb0, ya, yb, d0, d1, ex);
                             } else {
-                                span4_mma_x2(reinterpret_cast<const uint4*>(sp)[lane], P, xa0, xb0,
-                                             ya0, yb0, d0, d1, e0, e1);
+                                span4_mma_xn<NX>(reinterpret_cast<const uint4*>(sp)[lane], P, xa0,
+                                                 xb0, ya, yb, d0, d1, ex);
                             }
                             sp += UW;
                             xs += kSpanCols;
                         }
                     }
-                    if constexpr (BITS == 3 && NB != 4) {
+                    if constexpr (BITS == 3 && NB < 4) {
                         // span pairs: two independent units per iteration
                         for (; k + 1 < s_end; k += 2) {
                             const uint32_t a0 = sp[lane], a1 = sp[32 + lane], a2 = sp[64 + lane];
@@ -812,16 +825,21 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static bool attr_done[12][64] = {};
+    static bool attr_done[14][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     const int ci = p.consumers == 8 ? 0 : 1;
-    const int bi = (p.nbatch == 4 ? 8 : p.nbatch == 2 ? 4 : 0) + (p.bits == 3 ? 0 : 1) * 2 + ci;
+    // nbatch 8 has only 8-consumer kernels (the accumulators of four vector
+    // pairs need the registers)
+    const int bi = p.nbatch == 8 ? 12 + (p.bits == 3 ? 0 : 1)
+                                 : (p.nbatch == 4 ? 8 : p.nbatch == 2 ? 4 : 0) +
+                                       (p.bits == 3 ? 0 : 1) * 2 + ci;
     using K = void (*)(StackParams);
-    static const K kerns[12] = {
+    static const K kerns[14] = {
         stack_gemv<3, 8, 1>, stack_gemv<3, 16, 1>, stack_gemv<4, 8, 1>, stack_gemv<4, 16, 1>,
         stack_gemv<3, 8, 2>, stack_gemv<3, 16, 2>, stack_gemv<4, 8, 2>, stack_gemv<4, 16, 2>,
-        stack_gemv<3, 8, 4>, stack_gemv<3, 16, 4>, stack_gemv<4, 8, 4>, stack_gemv<4, 16, 4>};
+        stack_gemv<3, 8, 4>, stack_gemv<3, 16, 4>, stack_gemv<4, 8, 4>, stack_gemv<4, 16, 4>,
+        stack_gemv<3, 8, 8>, stack_gemv<4, 8, 8>};
     const K kern = kerns[bi];
     if (dev < 0 || dev >= 64 || !attr_done[bi][dev]) {
         int max_optin = 0;

@@ -131,30 +131,31 @@ __device__ __forceinline__ void span3_mma_one(uint32_t w0, uint32_t w1, uint32_t
     }
 }
 
-// batch 3..4: the same A fragments against a second x set (vectors 2/3)
-// into a second accumulator pair -- decode paid once for four vectors
-__device__ __forceinline__ void span3_mma_x2(uint32_t w0, uint32_t w1, uint32_t w2,
+// batch 3..8: the same A fragments against NX more x sets (vector pairs
+// 2/3, 4/5, 6/7) into NX more accumulator pairs -- decode paid once
+template <int NX>
+__device__ __forceinline__ void span3_mma_xn(uint32_t w0, uint32_t w1, uint32_t w2,
                                              const Planes8& P, const uint4& xa, const uint4& xb,
-                                             const uint4& ya, const uint4& yb, float (&d0)[4],
-                                             float (&d1)[4], float (&e0)[4], float (&e1)[4]) {
+                                             const uint4 (&ya)[NX], const uint4 (&yb)[NX],
+                                             float (&d0)[4], float (&d1)[4],
+                                             float (&e)[NX][2][4]) {
     const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
     const uint32_t t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) |
                        ((w2 >> 1) & 0x44444444u);
     const uint32_t sA[4] = {m0, hi16(m0), m1, hi16(m1)};
     const uint32_t sB[4] = {m2, hi16(m2), t, hi16(t)};
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-    const uint32_t ys[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         uint32_t a0, a1, a2, a3;
         quad8(sA[j], P, a0, a2);
         quad8(sB[j], P, a1, a3);
-        if (j & 1) {
-            hmma16816(d1, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-            hmma16816(e1, a0, a1, a2, a3, ys[2 * j], ys[2 * j + 1]);
-        } else {
-            hmma16816(d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-            hmma16816(e0, a0, a1, a2, a3, ys[2 * j], ys[2 * j + 1]);
+        hmma16816((j & 1) ? d1 : d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const uint4& A = (j < 2) ? ya[q] : yb[q];
+            const uint32_t y0 = (j & 1) ? A.z : A.x, y1 = (j & 1) ? A.w : A.y;
+            hmma16816(e[q][j & 1], a0, a1, a2, a3, y0, y1);
         }
     }
 }
@@ -187,10 +188,11 @@ __device__ __forceinline__ void span4_mma(const uint4& w, const Planes16& P, con
     }
 }
 
-__device__ __forceinline__ void span4_mma_x2(const uint4& w, const Planes16& P, const uint4& xa,
-                                             const uint4& xb, const uint4& ya, const uint4& yb,
-                                             float (&d0)[4], float (&d1)[4], float (&e0)[4],
-                                             float (&e1)[4]) {
+template <int NX>
+__device__ __forceinline__ void span4_mma_xn(const uint4& w, const Planes16& P, const uint4& xa,
+                                             const uint4& xb, const uint4 (&ya)[NX],
+                                             const uint4 (&yb)[NX], float (&d0)[4],
+                                             float (&d1)[4], float (&e)[NX][2][4]) {
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
     uint32_t sl[4], pk[4];
 #pragma unroll
@@ -199,7 +201,6 @@ __device__ __forceinline__ void span4_mma_x2(const uint4& w, const Planes16& P, 
         pk[q] = ((ws[q] >> 1) & 0x44444444u) | 0x32103210u;
     }
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-    const uint32_t ys[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int wa = j >> 1, wb = 2 + (j >> 1);
@@ -210,12 +211,12 @@ __device__ __forceinline__ void span4_mma_x2(const uint4& w, const Planes16& P, 
         uint32_t a0, a1, a2, a3;
         quad16(sa, pa, P, a0, a2);
         quad16(sb, pb, P, a1, a3);
-        if (j & 1) {
-            hmma16816(d1, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-            hmma16816(e1, a0, a1, a2, a3, ys[2 * j], ys[2 * j + 1]);
-        } else {
-            hmma16816(d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-            hmma16816(e0, a0, a1, a2, a3, ys[2 * j], ys[2 * j + 1]);
+        hmma16816((j & 1) ? d1 : d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const uint4& A = (j < 2) ? ya[q] : yb[q];
+            const uint32_t y0 = (j & 1) ? A.z : A.x, y1 = (j & 1) ? A.w : A.y;
+            hmma16816(e[q][j & 1], a0, a1, a2, a3, y0, y1);
         }
     }
 }
