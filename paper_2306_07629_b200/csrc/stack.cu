@@ -58,7 +58,10 @@ namespace sqz {
 // and re-reading them per field from every warp is slow.
 constexpr uint32_t kDescSlots = 8;
 constexpr uint32_t kWarpSlots = 2;  // ring slots per consumer warp
-constexpr uint32_t kCsrWarps = 4;   // warps that process the CSR deltas
+// CSR warps: p.csr_warps (1..kCsrWarps) process the CSR deltas -- chosen per
+// plan from the largest per-CTA entry count (each extra role warp costs the
+// decoding warps issue slots, so light outlier loads get fewer)
+constexpr uint32_t kCsrWarps = 4;
 struct __align__(16) SDesc {
     StackLayerDesc d;
     uint32_t e0, e1;  // CSR entries of this CTA's rows: [e0, e1)
@@ -216,13 +219,13 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         for (int b = 0; b < 2; ++b) {
             mbar_init(&xfull[b], 1);
             mbar_init(&cfull[b], 1);
-            mbar_init(&bempty[b], NC + 1 + kCsrWarps);
-            mbar_init(&pfull[b], NC + kCsrWarps);
-            mbar_init(&pempty[b], 1 + kCsrWarps);
+            mbar_init(&bempty[b], NC + 1 + p.csr_warps);
+            mbar_init(&pfull[b], NC + p.csr_warps);
+            mbar_init(&pempty[b], 1 + p.csr_warps);
         }
         for (uint32_t k = 0; k < kDescSlots; ++k) {
             mbar_init(&dfull[k], 32);
-            mbar_init(&dempty[k], NC + 2 + kCsrWarps);
+            mbar_init(&dempty[k], NC + 2 + p.csr_warps);
         }
         fence_barrier_init();
     }
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
             if (d.dep != kNoDep) {
                 if (lane == 0) {
-                    DSQ_WD_POLL(ld_acquire_gpu(p.counters + d.dep) < G * (1 + kCsrWarps),
+                    DSQ_WD_POLL(ld_acquire_gpu(p.counters + d.dep) < G * (1 + p.csr_warps),
                                 "stack watchdog: cta %u layer %u dep %u counter %u\n", cta, l, d.dep,
                                 *(volatile const uint32_t*)(p.counters + d.dep));
                     DSQ_TRACE(l, kTrDepMet);
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     // warp order (warps that did not touch a row left 0) plus their CSR
     // rounds in round order, y is stored, and each finishing warp bumps the
     // layer's completion counter (target grid * kFin)
-    constexpr uint32_t kFin = 1 + kCsrWarps;
+    const uint32_t kFin = 1 + p.csr_warps;
     auto finish_rows = [&](uint32_t l, uint32_t f) {
         const uint32_t b = l & 1u, ph = (l >> 1) & 1u;
         const SDesc& sd = sdesc[l % kDescSlots];
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 for (int v = 0; v < NB; ++v)
                     if (v == 0 || uint32_t(v) < p.nvec)
                         csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh + v * p.xvec,
-                                   S + v * (staged ? p.seg_cap : p.gseg_cap), cw, kCsrWarps, lane);
+                                   S + v * (staged ? p.seg_cap : p.gseg_cap), cw, p.csr_warps, lane);
             }
             __syncwarp();
             if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrDone);
@@ -817,7 +820,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3((p.consumers + 3 + kCsrWarps) * 32);
+    cfg.blockDim = dim3((p.consumers + 3 + p.csr_warps) * 32);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

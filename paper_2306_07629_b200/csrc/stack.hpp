@@ -85,6 +85,7 @@ struct StackParams {
     uint32_t gseg_cap;
     uint32_t grid;            // CTAs (== SMs, all co-resident)
     uint32_t consumers;       // decode warps per CTA (+ producer, loader, finisher warps)
+    uint32_t csr_warps;       // CSR / finishing warps (1..4)
     // dynamic shared memory carve-up (byte offsets)
     uint32_t off_desc;               // 8 x 128-byte layer descriptor cache
     uint32_t off_ring, slot_bytes, n_slots;
