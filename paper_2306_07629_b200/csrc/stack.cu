@@ -5,35 +5,29 @@
 // the balance granularity is one tile and no output row is ever shared
 // between CTAs -> no global merge, no floating-point atomics).
 //
-// Warp roles (consumers take the low warp ids, control warps the top ones,
-// which the issue arbiter favours):
-//   consumers 0..NC-1: every ring chunk (a fixed number of (tile, 256-column
-//              span) units of the CTA's share) is split in equal contiguous
-//              unit ranges over the NC warps; per unit a lane decodes 32
-//              indices of one tile row with PRMT byte-plane lookups into fp16
-//              A fragments and 4 mma.sync m16n8k16 accumulate them against x
-//              in fp32 (tile.cuh).  When a warp moves to another tile its D
-//              fragments collapse to the tile's 4 row partials, added into the
-//              warp's column of a shared-memory [warp][row] partial table.
-//              The CSR deltas of the CTA's rows are shared by the warps in
-//              32-entry rounds (segmented warp scan, host-built row-start
-//              bitmap); half of the warps do them before their dense units,
-//              half after, so the rounds' latency overlaps dense work.
-//   producer  (NC):   publishes each layer's descriptor to a shared-memory
-//              cache and streams the CTA's index units of layer 0, 1, 2, ...
-//              HBM -> shared-memory ring with cp.async.bulk (TMA bulk
-//              engine), completion on mbarriers.  Weights never depend on x,
-//              so it runs ahead across layer boundaries, bounded only by the
-//              ring -- the HBM pipe stays busy while other warps wait on a
-//              layer dependency.
+// Warp roles:
+//   consumers 0..NC-1: each owns a contiguous range of the CTA's (tile,
+//              256-column span) units of every layer and streams it through a
+//              private 2-slot TMA ring (cp.async.bulk, mbarrier completion)
+//              that runs ahead across layer boundaries (weights never depend
+//              on x).  Per unit a lane decodes 32 indices of one tile row with
+//              PRMT byte-plane lookups into fp16 A fragments and 4
+//              mma.sync.m16n8k16 accumulate them against x in fp32 (tile.cuh);
+//              on a tile change the D fragments collapse to the tile's 4 row
+//              partials in the warp's column of a [warp][row] smem table.
+//   publisher (NC): copies each layer's descriptor (+ the CTA's tile share
+//              and CSR range) into an 8-slot shared-memory cache.
 //   loader    (NC+1): stages the CTA's LUT planes, CSR slice (row_ptr,
 //              entries, row-start bitmap) and, once the layer producing x is
 //              complete on ALL CTAs (grid-wide completion counter,
-//              ld.acquire), the activation vector x -- all by TMA into
+//              ld.acquire), the activation vector(s) x -- all by TMA into
 //              double-buffered shared memory.
-//   finisher  (NC+2): per row, the dense partials in warp order plus the
-//              row's CSR round results in round order (deterministic), the
-//              store of y, and the layer's completion signal (red.release).
+//   finisher  (NC+2) and CSR warps (NC+3 ..): the CSR warps scan the CTA's
+//              deltas (segmented warp scans, host-built row-start bitmap)
+//              while the consumers decode; then all of them finish rows: the
+//              dense partials in warp order plus the row's CSR round results
+//              in round order (deterministic), the store of y (or the TP
+//              exchange), and the layer's completion signal (red.release).
 // Reference semantics: per row, LUT dot + CSR delta dot == fused_dns_matvec
 // (reference kernels.cpp:108-141); the hybrid split is unnecessary because the
 // CSR rounds are balanced regardless of per-row skew.
