@@ -547,8 +547,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     }
 
     // ---------------- consumers: dense LUT products ----------------------------
-    pdl_wait();
-    pdl_trigger();
+    // (the first ring chunks are requested before the PDL wait: the weights
+    // are launch constants, so their HBM latency overlaps the previous
+    // kernel's tail; everything that reads x or writes shared state waits)
     const uint32_t cw = warp;
     // this lane's B-column x halves (NB == 2: B columns 4..7, lanes 16..31,
     // read batch vector 1)
@@ -596,6 +597,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         }
     };
     for (uint32_t k = 0; k < WS; ++k) issue_next();
+    pdl_wait();
+    pdl_trigger();
     // dev profile (build with -DDSQ_STACK_PROFILE, run with DSQ_STACK_DBG bit
     // 2): cycles per consumer warp spent waiting for x / partial buffers,
     // waiting for ring data, decoding, and at layer boundaries
