@@ -263,7 +263,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
 
     if (warp == NC + 1) {
         // ---------------- loader: LUT planes, CSR slice, x (the dependency) ---
-        pdl_wait();
+        // layer 0's LUT planes are launch constants and go before the PDL
+        // wait; x (possibly the previous kernel's output) goes after it
         pdl_trigger();
         for (uint32_t l = 0; l < p.n_layers; ++l) {
             const uint32_t b = l & 1u;
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             // one shared x buffer (large batched stacks, p.x_step == 0): layer
             // l may overwrite x only after every reader of layer l-1's x is done
             if (p.x_step == 0 && l >= 1) mbar_wait(&bempty[(l - 1) & 1u], ((l - 1) >> 1) & 1u);
+            if (l == 0) pdl_wait();
             if (d.dep == kNoDep) stage_x();  // external input: no wait at all
             // row_ptr slice + CSR entries + row-start bitmap of the CTA's rows:
             // TMA bulk copies (16-byte granules; the device arrays are padded),
