@@ -228,9 +228,10 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
         max_rows = std::max(max_rows, ceil_div(Ls[i].tiles, G) * kTileRows);
         max_nnz = std::max(max_nnz, Ls[i].max_nnz_cta);
     }
-    // CSR warps: 2 while every CTA's entries fit the staged buffer twice over
-    // (the 0.05-0.45% outlier loads), 4 for heavier loads (DSQ_STACK_CSR_WARPS: dev)
-    sp.csr_warps = max_nnz <= 4096 ? 2u : 4u;
+    // CSR warps: 2 while a CTA's CSR work (entries x batch vectors, each
+    // vector is one scan) stays small -- the 0.05-0.45% outlier loads at
+    // batch 1 -- else 4 (DSQ_STACK_CSR_WARPS: dev override)
+    sp.csr_warps = uint64_t(max_nnz) * nbatch <= 1536 ? 2u : 4u;
     if (const char* e = std::getenv("DSQ_STACK_CSR_WARPS")) {
         const int c = atoi(e);
         if (c >= 1 && c <= 4) sp.csr_warps = uint32_t(c);
