@@ -603,7 +603,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     pdl_trigger();
     // dev profile (build with -DDSQ_STACK_PROFILE, run with DSQ_STACK_DBG bit
     // 2): cycles per consumer warp spent waiting for x / partial buffers,
-    // waiting for ring data, decoding, and at layer boundaries
+    // waiting for ring data, in chunk / segment bookkeeping ("dense"), in the
+    // unit loops (slot 3), and at layer boundaries
 #ifdef DSQ_STACK_PROFILE
     const bool prof = (p.dbg & 4u) && p.trace;
     long long c_xw = 0, c_fw = 0, c_dense = 0, c_csr = 0, c_top = 0, t_mark = clock64();
@@ -678,6 +679,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 for (int k = 0; k < 4; ++k) d0[k] = d1[k] = 0.f;
             }
         };
+        // (tile, span) of the next unit, carried across chunks (chunks are
+        // consecutive ranges): one division per layer, not per chunk
+        uint32_t tile_c = u0 / NS, s_c = u0 - tile_c * NS;
         for (uint32_t cb = u0; cb < u1; cb += cu) {
             DSQ_LAP(c_dense);
             if (!(p.dbg & 8u)) mbar_wait(&full[cw * WS + cslot], cphase);  // dbg 8: compute only
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             uint32_t u = cb;
             const uint32_t ue = min(u1, cb + cu);
             if (!(p.dbg & 1u)) {
-                uint32_t tile = u / NS, s = u - tile * NS;
+                uint32_t tile = tile_c, s = s_c;
                 const uint32_t* sp = chunk;
                 while (u < ue) {
                     if (tile != cur_tile) {
@@ -703,6 +707,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                     // spans [s, s_end) of this tile; software-pipelined: the
                     // next span's words and x are loaded before the current
                     // span is decoded
+                    DSQ_LAP(c_dense);  // (profile: segment set-up counts as dense)
                     const uint32_t s_end = min(NS, s + (ue - u));
                     const uint16_t* xs = xh + s * kSpanCols + xoff;
                     uint32_t w[BITS];
@@ -777,6 +782,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                             span4_mma(make_uint4(wc[0], wc[1], wc[2], wc[3]), P, xac, xbc, d0, d1);
                         }
                     }
+                    DSQ_LAP(c_csr);  // (profile slot 3: the unit loops themselves)
                     u += s_end - s;
                     s = s_end;
                     if (s == NS) {
@@ -784,6 +790,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         s = 0;
                     }
                 }
+                tile_c = tile;
+                s_c = s;
             }
             // the slot's words are consumed (their values were used): refill
             // it with the next chunk of this warp's stream
@@ -792,7 +800,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 cslot = 0;
                 cphase ^= 1u;
             }
+            DSQ_LAP(c_dense);
             issue_next();
+            DSQ_LAP(c_fw);  // (profile: the refill issue counts with the ring wait)
         }
         flush();
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrDenseDone);

@@ -48,14 +48,14 @@ def main():
     got = lib.dsq_cuda_stack_trace(st.handle, buf.ctypes.data, buf.size)
     assert got, "trace buffer missing"
     prof = buf[: G * NC * 5].reshape(G, NC, 5).astype(np.float64)
-    names = ["x/part wait", "ring wait", "dense", "csr", "layer top"]
+    names = ["x/part wait", "ring wait", "chunk/segment bookkeeping", "unit loops", "layer top"]
     tot = prof.sum(axis=2).mean()
     print(f"{rows}x{cols} b{bits} sp{sp} x{n}: {ms * 1e3 / n:.2f} us/layer; consumer cycles/layer "
           f"(mean over CTAs, warps): " + ", ".join(
               f"{nm} {prof[:, :, k].mean() / n:.0f} ({prof[:, :, k].mean() / tot * 100:.0f}%)"
               for k, nm in enumerate(names)))
-    w = prof[:, :, 2].mean(axis=0) / n
-    print("  dense cycles/layer per warp:", " ".join(f"{v:.0f}" for v in w))
+    w = (prof[:, :, 2] + prof[:, :, 3]).mean(axis=0) / n
+    print("  dense (bookkeeping + loops) cycles/layer per warp:", " ".join(f"{v:.0f}" for v in w))
 
 
 if __name__ == "__main__":
