@@ -216,7 +216,15 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     int dev = 0, smax = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    sp.consumers = kStackConsumersDefault;
+    // consumer warps: every warp pays a fixed cost per layer (descriptor,
+    // chunk and tile bookkeeping, the HMMA drain at tile changes), so stacks
+    // whose layers give a CTA few units (LLaMA-7B 4096-row layers: ~111) run
+    // better with 8 consumer warps (twice the units each), big layers with 16
+    {
+        uint64_t units = 0;
+        for (uint32_t i = 0; i < n; ++i) units += uint64_t(ceil_div(Ls[i].tiles, G)) * Ls[i].ns;
+        sp.consumers = units <= 200ull * n ? 8u : kStackConsumersDefault;
+    }
     if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
         const int c = atoi(e);
         if (c == 8 || c == 16) sp.consumers = uint32_t(c);
