@@ -528,8 +528,18 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
     setup_s = time.time() - t_setup
     sampler = ClockSampler(local_rank)
     sampler.start()
-    for _ in range(max(1, int(args.soak * 20))):
+    # soak for ~args.soak seconds; the run count is agreed across ranks so the
+    # fused-reduce launches stay paired
+    t0 = time.time()
+    s_warm.run(sp)
+    torch.cuda.synchronize()
+    per_run = max(time.time() - t0, 1e-5)
+    n_soak = torch.tensor([int(args.soak / per_run) + 1], device=dev, dtype=torch.int64)
+    dist.all_reduce(n_soak, op=dist.ReduceOp.MAX)
+    for i in range(int(n_soak.item())):
         s_warm.run(sp)
+        if i % 64 == 63:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     s_warm.run(sp)
     dist.barrier()
