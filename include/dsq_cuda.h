@@ -207,17 +207,23 @@ typedef struct dsq_cuda_stack dsq_cuda_stack;
 int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
                           const void* const* xs, void* const* ys, int y_dtype,
                           dsq_cuda_stack** out);
-/* A stack over `batch` (1..4) activation vectors at once (serving several
+/* A stack over `batch` (1..16) activation vectors at once (serving several
  * sequences): vector v of layer i's input is xs[i] + v * x_bstride halves
  * (external inputs) or its producer's output vector v; vector v of the output
  * is ys[i] + v * y_bstride elements (strides multiples of 8, >= the largest
  * cols / rows).  Every decoded weight is shared by all vectors (batch 2: the
- * spare HMMA B columns; 3..4: a second HMMA per fragment).  Single GPU. */
+ * spare HMMA B columns; 3..4: a second HMMA per fragment).  Batches of 5..16,
+ * or of 2..4 whose x vectors do not fit next to the persistent kernel's ring,
+ * run in the sequential form: one batched product launch per layer, back to
+ * back under programmatic dependent launch (dsq_cuda_stack_info).  Single GPU. */
 int dsq_cuda_stack_create_batch(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
                                 const void* const* xs, void* const* ys, int y_dtype,
                                 uint32_t batch, uint32_t x_bstride, uint32_t y_bstride,
                                 dsq_cuda_stack** out);
 int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
+/* persistent = 1 when the whole stack runs as one persistent launch, 0 for the
+ * sequential form; launches = kernel launches of the last run (1 persistent). */
+int dsq_cuda_stack_info(const dsq_cuda_stack* stack, uint32_t* persistent, uint32_t* launches);
 /* one decode step from host buffers: copy x_host (x_bytes, pinned for async)
  * into x_dev (the stack's external input), run the stack, copy y_dev into
  * y_host, synchronise the stream.  A 0 byte count skips that copy. */

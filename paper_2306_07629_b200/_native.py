@@ -141,6 +141,7 @@ PROTOTYPES = {
                                         C.POINTER(C.c_void_p)]),
     "dsq_cuda_stack_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_stack_destroy": (C.c_int, [C.c_void_p]),
+    "dsq_cuda_stack_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "dsq_cuda_tp_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                      C.POINTER(C.c_void_p), C.c_void_p]),
     "dsq_cuda_tp_connect": (C.c_int, [C.c_void_p, C.c_void_p]),

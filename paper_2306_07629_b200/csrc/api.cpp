@@ -336,7 +336,11 @@ struct dsq_cuda_layer {
     uint32_t* stack_counters = nullptr;     // [2]
     float* gseg1 = nullptr;
     StackParams sp2{}, sp4{}, sp8{};        // batch 2 / 3..4 / 5..8 single-layer plans (lazy)
-    bool sp2_ready = false, sp4_ready = false, sp8_ready = false, sp8_failed = false;
+    bool sp2_ready = false, sp4_ready = false, sp8_ready = false;
+    bool sp2_failed = false, sp4_failed = false, sp8_failed = false;  // x does not fit: K8
+    bool k7_batch_failed(uint32_t nb) const {
+        return nb == 2 ? sp2_failed : nb == 4 ? sp4_failed : sp8_failed;
+    }
     float* gseg2 = nullptr;
     float* gseg4 = nullptr;
     float* gseg8 = nullptr;
@@ -775,14 +779,15 @@ static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
 
 // batched products (K8, batch.cu): x [batch][cols] fp16, y [batch][rows]
 static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype, void* y,
-                      int y_dtype, uint32_t batch, cudaStream_t st) {
+                      int y_dtype, uint32_t batch, cudaStream_t st, uint32_t x_stride,
+                      uint32_t y_stride) {
     if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_FUSED)
         return fail(DSQ_E_UNSUPPORTED, "batched products: LUT, CSR or FUSED kernels");
     if (!L->rec_layout)
         return fail(DSQ_E_UNSUPPORTED, "batched products need bits 3 or 4 (got %u)", L->bits);
     if (x_dtype != DSQ_F16) return fail(DSQ_E_INVALID_ARGUMENT, "batched x must be F16");
-    if ((reinterpret_cast<uintptr_t>(x) & 15u) || (L->cols % 8))
-        return fail(DSQ_E_INVALID_ARGUMENT, "batched x rows must be 16-byte aligned (cols %% 8 == 0)");
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) || (x_stride % 8))
+        return fail(DSQ_E_INVALID_ARGUMENT, "batched x rows must be 16-byte aligned (stride %% 8 == 0)");
     if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
         return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
     {
@@ -794,28 +799,34 @@ static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype,
             const uint32_t want = std::max<uint32_t>(1, ceil_div(4u * uint32_t(L->num_sms), groups));
             L->batch_spans = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(L->ns, want), 2));
             L->batch_kslices = ceil_div(L->ns, L->batch_spans);
+            // + the transposed x [ns * 256 cols][16] halves for the CSR gathers
             CUDA_TRY(cudaMalloc(&L->batch_part,
-                                size_t(L->batch_kslices) * tiles16 * 16 * 16 * sizeof(float)));
+                                size_t(L->batch_kslices) * tiles16 * 16 * 16 * sizeof(float) +
+                                    size_t(L->ns) * kSpanCols * 16 * sizeof(uint16_t)));
         }
     }
     const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
     CUDA_TRY(launch_batch(L->bits, L->rec, L->tlut, L->P.row_ptr, L->P.csr, L->rows, L->cols,
-                          L->ns, L->tiles, static_cast<const uint16_t*>(x), L->cols, batch, y,
-                          L->rows, y_dtype == DSQ_F16, L->batch_part, L->batch_kslices,
+                          L->ns, L->tiles, static_cast<const uint16_t*>(x), x_stride, batch, y,
+                          y_stride, y_dtype == DSQ_F16, L->batch_part, L->batch_kslices,
                           L->batch_spans, mode, st));
     return DSQ_OK;
 }
 
+// x_stride / y_stride: elements between the batch's vectors (0: cols / rows)
 static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_dtype, void* y,
-                     int y_dtype, uint32_t batch, cudaStream_t st, bool pdl) {
+                     int y_dtype, uint32_t batch, cudaStream_t st, bool pdl,
+                     uint32_t x_stride = 0, uint32_t y_stride = 0) {
     auto* L = const_cast<dsq_cuda_layer*>(Lc);
     if (!L || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (!x_stride) x_stride = L->cols;
+    if (!y_stride) y_stride = L->rows;
     if (batch < 1 || batch > 16) return fail(DSQ_E_INVALID_ARGUMENT, "batch must be 1..16");
     const uint32_t nbk = batch == 2 ? 2u : batch <= 4 ? 4u : 8u;
-    if (batch >= 2 && batch <= 8 && L->rec_layout && !(nbk == 8 && L->sp8_failed) &&
+    if (batch >= 2 && batch <= 8 && L->rec_layout && !L->k7_batch_failed(nbk) &&
         (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
         x_dtype == DSQ_F16 && (y_dtype == DSQ_F32 || y_dtype == DSQ_F16) &&
-        !(reinterpret_cast<uintptr_t>(x) & 15u) && L->cols % 8 == 0) {
+        !(reinterpret_cast<uintptr_t>(x) & 15u) && x_stride % 8 == 0) {
         // K7 with 2 or 4 activation vectors in one launch: all share every
         // decoded weight fragment (vectors 0/1 in the HMMA B columns 0..3 /
         // 4..7, vectors 2/3 in a second HMMA on the same A fragment)
@@ -830,8 +841,8 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
                 StackPlanLayer pl{L->rows, L->cols, L->tiles, L->ns,
                                   max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
                 int prc = plan_stack(&pl, 1, L->num_sms, L->bits, spb, gcap, nb);
-                if (prc && nb == 8) {  // 8 x vectors do not fit: the K8 path
-                    L->sp8_failed = true;
+                if (prc == DSQ_E_UNSUPPORTED) {  // the x vectors do not fit: the K8 path
+                    (nb == 2 ? L->sp2_failed : nb == 4 ? L->sp4_failed : L->sp8_failed) = true;
                     goto batched_k8;
                 }
                 if (prc) return prc;
@@ -864,15 +875,16 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
             d.row_ptr = L->zero_rp;
             d.csr_rng = L->zero_rng;
         }
-        sp.x_bstride = L->cols;
-        sp.y_bstride = L->rows;
+        sp.x_bstride = x_stride;
+        sp.y_bstride = y_stride;
         sp.n_layers = 1;
         sp.layers = nullptr;
         CUDA_TRY(launch_stack(sp, st, pdl));
         return DSQ_OK;
     }
 batched_k8:
-    if (batch > 1) return gemv_batch(L, kernel, x, x_dtype, y, y_dtype, batch, st);
+    if (batch > 1)
+        return gemv_batch(L, kernel, x, x_dtype, y, y_dtype, batch, st, x_stride, y_stride);
     if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)
         return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);
     if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
@@ -1005,10 +1017,24 @@ struct dsq_cuda_tp {
     bool peer_ipc[8] = {};
 };
 
+// a stack step run as its own product launch (the sequential form)
+struct StackSeqStep {
+    const dsq_cuda_layer* layer;
+    const void* x;
+    void* y;
+    uint32_t x_stride, y_stride;
+};
+
 struct dsq_cuda_stack {
     int device = 0;
     uint32_t n = 0;
     uint32_t n_reduce = 0;
+    // sequential form: batches the persistent kernel cannot hold (5..16, or
+    // x vectors that do not fit next to the ring) run layer by layer through
+    // the batched product kernels, back to back under PDL
+    bool seq = false;
+    uint32_t batch = 1, y_dtype = DSQ_F16, launches = 1;
+    std::vector<StackSeqStep> steps;
     dsq_cuda_tp* tp = nullptr;
     StackParams sp{};
     void* arena = nullptr;
@@ -1023,8 +1049,8 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     if (!out || !layers || !deps || !xs || !ys || n == 0)
         return fail(DSQ_E_INVALID_ARGUMENT, "stack: null argument or empty stack");
     *out = nullptr;
-    if (batch < 1 || batch > 4)
-        return fail(DSQ_E_INVALID_ARGUMENT, "stack: batch must be 1..4");
+    if (batch < 1 || batch > 16)
+        return fail(DSQ_E_INVALID_ARGUMENT, "stack: batch must be 1..16");
     const uint32_t nbatch = batch == 1 ? 1u : batch == 2 ? 2u : 4u;
     if (batch > 1) {
         if (tp) return fail(DSQ_E_UNSUPPORTED, "stack: batched stacks are single-GPU");
@@ -1082,8 +1108,22 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     S->n = n;
     S->n_reduce = n_reduce;
     S->tp = tp;
+    S->batch = batch;
+    S->y_dtype = uint32_t(y_dtype);
     uint32_t gseg_cap = 0;
-    int rc = plan_stack(pl.data(), n, G, L0->bits, S->sp, gseg_cap, nbatch);
+    int rc = batch > 4 ? DSQ_E_UNSUPPORTED : plan_stack(pl.data(), n, G, L0->bits, S->sp, gseg_cap, nbatch);
+    if (rc == DSQ_E_UNSUPPORTED && !tp && !grid) {
+        // too many vectors for the persistent kernel: one product launch per layer
+        S->seq = true;
+        S->launches = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            const bool chained = deps[i] >= 0;
+            S->steps.push_back(StackSeqStep{layers[i], chained ? ys[deps[i]] : xs[i], ys[i],
+                                            chained ? y_bstride : x_bstride, y_bstride});
+        }
+        *out = S;
+        return DSQ_OK;
+    }
     if (rc) {
         delete S;
         return rc;
@@ -1305,6 +1345,19 @@ int dsq_cuda_stack_run_host(dsq_cuda_stack* S, const void* x_host, void* x_dev, 
 int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
     if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
     cudaSetDevice(S->device);
+    if (S->seq) {
+        uint32_t launches = 0;
+        for (const StackSeqStep& q : S->steps) {
+            const int rc = gemv_impl(q.layer, DSQ_KERNEL_FUSED, q.x, DSQ_F16, q.y, int(S->y_dtype),
+                                     S->batch, static_cast<cudaStream_t>(stream), true,
+                                     q.x_stride, q.y_stride);
+            if (rc) return rc;
+            const uint32_t nbk = S->batch == 2 ? 2u : S->batch <= 4 ? 4u : 8u;
+            launches += S->batch == 1 || (S->batch <= 8 && !q.layer->k7_batch_failed(nbk)) ? 1u : 2u;
+        }
+        S->launches = launches;
+        return DSQ_OK;
+    }
     if (S->tp) {
         // every rank runs the same sequence of launches, so the reduce
         // ordinals (and the peers' flag targets) stay in step
@@ -1312,6 +1365,13 @@ int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
         S->tp->base += S->n_reduce;
     }
     CUDA_TRY(launch_stack(S->sp, static_cast<cudaStream_t>(stream), true));
+    return DSQ_OK;
+}
+
+int dsq_cuda_stack_info(const dsq_cuda_stack* S, uint32_t* persistent, uint32_t* launches) {
+    if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
+    if (persistent) *persistent = S->seq ? 0u : 1u;
+    if (launches) *launches = S->launches;
     return DSQ_OK;
 }
 

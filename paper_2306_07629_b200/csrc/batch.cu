@@ -36,6 +36,7 @@ struct BatchParams {
     const uint32_t* lut;      // [tiles4][4][LW]
     const uint16_t* x;        // [B][cols] fp16, rows 16-byte aligned (x_stride halves)
     float* part;              // [kslices][rows16][B] fp32 partials
+    uint16_t* xT;             // [cols][8 * NB] x transposed (column-major batch), for the CSR pass
     uint32_t rows, cols, ns, tiles4, tiles16, B, x_stride;
     uint32_t kslices, spans_per_slice;
     uint32_t xs_stride;       // halves per batch row in smem (slice cols + 8 pad)
@@ -99,6 +100,15 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batch_gemv(const __grid_cons
         }
     }
     __syncthreads();
+    if (grp == 0 && p.xT) {
+        // the slice's x transposed: all batch values of a column in one 16- or
+        // 32-byte run, so the CSR pass gathers one sector per column, not per vector
+        const uint32_t nbv = 8 * NB;
+        for (uint32_t k = threadIdx.x; k < ccount * nbv; k += blockDim.x) {
+            const uint32_t c = k / nbv, b = k - c * nbv;
+            p.xT[size_t(c0 + c) * nbv + b] = xs[b * p.xs_stride + c];
+        }
+    }
     const uint32_t Q = grp * kBatchWarps + warp;  // 16-row tile
     if (Q >= p.tiles16) return;
     // the thread's two rows: A row g -> 4-row tile 4Q + g/4, A row g+8 -> 4Q + 2 + g/4
@@ -193,45 +203,60 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batch_gemv(const __grid_cons
     }
 }
 
-// y[b][r] = sum over slices (in order) + sum over the row's CSR deltas (in
-// order).  Loads are issued 8 at a time so the latency of the dependent
-// entry -> x loads is paid once per 8 entries.
+// y[b][r] = sum over slices (in order) + sum over the row's CSR deltas.  One
+// warp per row: lane = part * XB + b (XB = 8 or 16 batch slots, P = 32 / XB
+// parts); part k takes the row's entries in groups of 8, group j when
+// j % P == k, and the parts are added in a fixed shuffle order (deterministic).
+// Loads are issued 8 at a time so the latency of the dependent entry -> x
+// loads is paid once per 8 entries; with the transposed x (xT) the XB lanes of
+// one part read one column's batch values from one 16- / 32-byte run.
+template <int XB>
 __global__ void batch_finish(const float* __restrict__ part, uint32_t kslices, uint32_t rows16,
                              uint32_t rows, uint32_t B, const uint32_t* __restrict__ row_ptr,
                              const uint32_t* __restrict__ csr, const uint16_t* __restrict__ x,
-                             uint32_t x_stride, void* y, uint32_t y_stride, int y_f16,
-                             int with_dense, int with_csr) {
+                             uint32_t x_stride, const uint16_t* __restrict__ xT, void* y,
+                             uint32_t y_stride, int y_f16, int with_dense, int with_csr) {
+    constexpr uint32_t P = 32 / XB;
     pdl_trigger();
     pdl_wait();  // the partials of the preceding batch_gemv
-    const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= size_t(rows) * B) return;
-    const uint32_t r = uint32_t(id / B), b = uint32_t(id % B);
+    const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31, b = lane % XB, k = lane / XB;
+    if (r >= rows) return;  // whole warps
+    const bool live = b < B;
     float s = 0.f;
-    if (with_dense) {
-        uint32_t k = 0;
-        for (; k + 4 <= kslices; k += 4) {
-            float v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = part[(size_t(k + u) * rows16 * 16 + r) * B + b];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) s += v[u];
-        }
-        for (; k < kslices; ++k) s += part[(size_t(k) * rows16 * 16 + r) * B + b];
-    }
-    if (with_csr) {
-        const uint16_t* xb = x + size_t(b) * x_stride;
+    if (with_csr && live) {
+        // x[b][col] = xb[col * xs] (transposed copy from batch_gemv when present)
+        const uint16_t* xb = xT ? xT + b : x + size_t(b) * x_stride;
+        const uint32_t xs = xT ? uint32_t(XB) : 1u;
         const uint32_t q0 = row_ptr[r], q1 = row_ptr[r + 1];
-        for (uint32_t q = q0; q < q1; q += 8) {
+        for (uint32_t q = q0 + 8 * k; q < q1; q += 8 * P) {
             uint32_t e[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) e[u] = q + u < q1 ? __ldg(csr + q + u) : 0u;
             uint16_t xv[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) xv[u] = q + u < q1 ? __ldg(xb + (e[u] & 0xffffu)) : uint16_t(0);
+            for (int u = 0; u < 8; ++u)
+                xv[u] = q + u < q1 ? __ldg(xb + size_t(e[u] & 0xffffu) * xs) : uint16_t(0);
 #pragma unroll
             for (int u = 0; u < 8; ++u)
                 if (q + u < q1) s = fma_h(uint16_t(e[u] >> 16), xv[u], s);
         }
+    }
+#pragma unroll
+    for (uint32_t o = XB; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (k != 0 || !live) return;
+    if (with_dense) {
+        float d = 0.f;
+        uint32_t j = 0;
+        for (; j + 4 <= kslices; j += 4) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = part[(size_t(j + u) * rows16 * 16 + r) * B + b];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d += v[u];
+        }
+        for (; j < kslices; ++j) d += part[(size_t(j) * rows16 * 16 + r) * B + b];
+        s = d + s;
     }
     if (y_f16)
         static_cast<__half*>(y)[size_t(b) * y_stride + r] = __float2half_rn(s);
@@ -283,6 +308,11 @@ cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut
     p.spans_per_slice = spans_per_slice;
     p.xs_stride = spans_per_slice * kSpanCols + 8;
     const int with_dense = mode != 1, with_csr = mode != 0;
+    // the transposed x lives after the partials (api.cpp sizes the buffer)
+    p.xT = with_dense && with_csr
+               ? reinterpret_cast<uint16_t*>(part + size_t(kslices) * p.tiles16 * 16 * 16)
+               : nullptr;
+    const uint32_t xT_stride = B > 8 ? 16u : 8u;
     if (with_dense) {
         const uint32_t groups = (p.tiles16 + kBatchWarps - 1) / kBatchWarps;
         const size_t smem = batch_smem_bytes(B, spans_per_slice);
@@ -297,10 +327,15 @@ cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut
             cudaSuccess)
             return e;
     }
-    const size_t n = size_t(rows) * B;
-    return launch_pdl(batch_finish, dim3(uint32_t((n + 255) / 256)), dim3(256), 0, st, part,
-                      kslices, p.tiles16, rows, B, row_ptr, csr, x, x_stride, y, y_stride,
-                      y_f16 ? 1 : 0, with_dense, with_csr);
+    const dim3 fg((rows + 7) / 8), fb(256);  // one warp per row
+    const uint16_t* xT = p.xT;
+    return xT_stride == 16
+               ? launch_pdl(batch_finish<16>, fg, fb, 0, st, part, kslices, p.tiles16, rows, B,
+                            row_ptr, csr, x, x_stride, xT, y, y_stride, y_f16 ? 1 : 0, with_dense,
+                            with_csr)
+               : launch_pdl(batch_finish<8>, fg, fb, 0, st, part, kslices, p.tiles16, rows, B,
+                            row_ptr, csr, x, x_stride, xT, y, y_stride, y_f16 ? 1 : 0, with_dense,
+                            with_csr);
 }
 
 }  // namespace sqz

@@ -252,9 +252,11 @@ class DeviceStack:
     is layer i's x, or -1 for the external fp16 buffer xs[i] (device pointer).
     With ``tp`` (a TPContext), layers with reduce[i] produce partial sums that
     the kernel all-reduces over the ranks' peer memory (dsq_cuda_stack_create_tp);
-    ``grid`` = CTAs (0: one per SM).  ``batch`` (1..4) activation vectors at
+    ``grid`` = CTAs (0: one per SM).  ``batch`` (1..16) activation vectors at
     once: vector v of an external x at xs[i] + v * x_stride halves, of every
-    output at ys[i] + v * y_stride elements (dsq_cuda_stack_create_batch)."""
+    output at ys[i] + v * y_stride elements (dsq_cuda_stack_create_batch).
+    Batches the persistent kernel cannot hold run in the sequential form (one
+    batched product launch per layer): see ``persistent`` / ``launches``."""
 
     def __init__(self, layers: list, deps: list, xs: list, ys: list, y_dtype: int,
                  reduce: list | None = None, tp: "TPContext | None" = None, grid: int = 0,
@@ -284,6 +286,21 @@ class DeviceStack:
 
     def run(self, stream: int = 0) -> None:
         check(lib.dsq_cuda_stack_run(self.handle, stream))
+
+    def _info(self) -> tuple[int, int]:
+        p, n = C.c_uint32(), C.c_uint32()
+        check(lib.dsq_cuda_stack_info(self.handle, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    @property
+    def persistent(self) -> bool:
+        """True when the whole stack is one persistent launch."""
+        return bool(self._info()[0])
+
+    @property
+    def launches(self) -> int:
+        """Kernel launches of the last run (1 for the persistent form)."""
+        return self._info()[1]
 
     def run_host(self, x_host: int, x_dev: int, x_bytes: int, y_dev: int, y_host: int,
                  y_bytes: int, stream: int = 0) -> None:

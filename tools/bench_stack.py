@@ -17,7 +17,7 @@ tensor-parallel (configs[3]): v,q,k,up,gate column-parallel, o,down
 row-parallel, the two all-reduces per decoder layer fused into the stack
 kernel over NVLink peer memory; timing is the max over ranks.
 
-usage: python tools/bench_stack.py [--model 13b] [--tokens 3] [--rotation 8] [--batch 1..4]
+usage: python tools/bench_stack.py [--model 13b] [--tokens 3] [--rotation 8] [--batch 1..16]
        torchrun --nproc-per-node 8 tools/bench_stack.py --model 65b
 """
 import argparse
@@ -143,6 +143,7 @@ def run(model, tokens, rotation, peak, rank=0, world=1, batch=1):
     return {
         "model": f"llama-{model} linear stack ({nl} decoder layers x 7 GEMVs, 3-bit + 0.45% CSR)",
         "tokens": tokens, "gpus": world, "parallelism": f"tp{world}", "batch": batch,
+        "form": "persistent" if timed.persistent else f"sequential ({timed.launches} launches)",
         "us_per_gemv": round(ms * 1e3 / gemvs, 3),
         "ms_per_token": round(ms / tokens, 4),
         "decode_tok_s_linear": round(batch * tokens / (ms * 1e-3), 1),
@@ -156,7 +157,7 @@ def main():
     ap.add_argument("--model", default="13b", choices=list(MODELS) + ["all"])
     ap.add_argument("--tokens", type=int, default=3)
     ap.add_argument("--rotation", type=int, default=8)
-    ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1..4)")
+    ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1..16)")
     args = ap.parse_args()
     try:
         peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
