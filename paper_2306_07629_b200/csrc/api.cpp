@@ -798,6 +798,7 @@ static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype,
             const uint32_t tiles16 = (L->tiles + 3) / 4, groups = (tiles16 + 7) / 8;
             const uint32_t want = std::max<uint32_t>(1, ceil_div(4u * uint32_t(L->num_sms), groups));
             L->batch_spans = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(L->ns, want), 2));
+            if (const char* e = std::getenv("DSQ_K8_SPANS")) L->batch_spans = std::max(1, atoi(e));
             L->batch_kslices = ceil_div(L->ns, L->batch_spans);
             // + the transposed x [ns * 256 cols][16] halves for the CSR gathers
             CUDA_TRY(cudaMalloc(&L->batch_part,

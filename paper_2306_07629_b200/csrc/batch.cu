@@ -83,34 +83,10 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batch_gemv(const __grid_cons
     const uint32_t s1 = min(p.ns, s0 + p.spans_per_slice);
     const uint32_t c0 = s0 * kSpanCols;
     const uint32_t ccount = min(p.cols, s1 * kSpanCols) - min(p.cols, c0);
-    // x and the partial buffer may belong to the previous launch on this
-    // stream (programmatic dependent launch): wait for it first
-    pdl_trigger();
-    pdl_wait();
-    // stage the slice's x for all 8*NB B-columns (zero beyond B and cols),
-    // 16 bytes per load (x rows are 16-byte aligned, cols % 8 == 0)
-    {
-        const uint32_t per_row = (s1 - s0) * kSpanCols / 8;  // uint4 per batch row
-        for (uint32_t k = threadIdx.x; k < 8 * NB * per_row; k += blockDim.x) {
-            const uint32_t b = k / per_row, c = (k - b * per_row) * 8;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (b < p.B && c < ccount)
-                v = __ldg(reinterpret_cast<const uint4*>(p.x + size_t(b) * p.x_stride + c0 + c));
-            *reinterpret_cast<uint4*>(xs + b * p.xs_stride + c) = v;
-        }
-    }
-    __syncthreads();
-    if (grp == 0 && p.xT) {
-        // the slice's x transposed: all batch values of a column in one 16- or
-        // 32-byte run, so the CSR pass gathers one sector per column, not per vector
-        const uint32_t nbv = 8 * NB;
-        for (uint32_t k = threadIdx.x; k < ccount * nbv; k += blockDim.x) {
-            const uint32_t c = k / nbv, b = k - c * nbv;
-            p.xT[size_t(c0 + c) * nbv + b] = xs[b * p.xs_stride + c];
-        }
-    }
+    // the weights are immutable: the LUT planes and the first span's index
+    // words are requested before the PDL wait and the x staging, so their
+    // DRAM latency overlaps both
     const uint32_t Q = grp * kBatchWarps + warp;  // 16-row tile
-    if (Q >= p.tiles16) return;
     // the thread's two rows: A row g -> 4-row tile 4Q + g/4, A row g+8 -> 4Q + 2 + g/4
     const uint32_t T0 = 4 * Q + (g >> 2), T1 = T0 + 2;
     const bool v0 = T0 < p.tiles4, v1 = T1 < p.tiles4;
@@ -149,6 +125,33 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batch_gemv(const __grid_cons
         }
     };
     if (s0 < s1) fetch(s0);
+    // x and the partial buffer may belong to the previous launch on this
+    // stream (programmatic dependent launch): wait for it first
+    pdl_trigger();
+    pdl_wait();
+    // stage the slice's x for all 8*NB B-columns (zero beyond B and cols),
+    // 16 bytes per load (x rows are 16-byte aligned, cols % 8 == 0)
+    {
+        const uint32_t per_row = (s1 - s0) * kSpanCols / 8;  // uint4 per batch row
+        for (uint32_t k = threadIdx.x; k < 8 * NB * per_row; k += blockDim.x) {
+            const uint32_t b = k / per_row, c = (k - b * per_row) * 8;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (b < p.B && c < ccount)
+                v = __ldg(reinterpret_cast<const uint4*>(p.x + size_t(b) * p.x_stride + c0 + c));
+            *reinterpret_cast<uint4*>(xs + b * p.xs_stride + c) = v;
+        }
+    }
+    __syncthreads();
+    if (grp == 0 && p.xT) {
+        // the slice's x transposed: all batch values of a column in one 16- or
+        // 32-byte run, so the CSR pass gathers one sector per column, not per vector
+        const uint32_t nbv = 8 * NB;
+        for (uint32_t k = threadIdx.x; k < ccount * nbv; k += blockDim.x) {
+            const uint32_t c = k / nbv, b = k - c * nbv;
+            p.xT[size_t(c0 + c) * nbv + b] = xs[b * p.xs_stride + c];
+        }
+    }
+    if (Q >= p.tiles16) return;
     for (uint32_t s = s0; s < s1; ++s) {
         const uint32_t sl = (s - s0) * kSpanCols;
         uint32_t wc[2][2][BITS];
