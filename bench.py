@@ -366,7 +366,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": SHAPES[-1][1] * 2,
                "steps": n_e2e, "ms_per_step": round(el / n_e2e * 1e3, 4),
                "api": "DeviceStack.run_host (dsq_cuda_stack_run_host) per decoder-layer step: "
-                      "pinned host x -> device (async copy), the 7-GEMV stack writing the step "
+                      "pinned host x -> device (read by a 1-CTA upload kernel whose PCIe latency "
+                      "overlaps the stack kernel's weight prologue under PDL), the 7-GEMV stack writing the step "
                       "output straight into pinned host memory (zero-copy), stream synchronised "
                       "every step"}
         # the reference-signature host call, per GEMV (fp32 host x -> fp64 host y,

@@ -224,9 +224,12 @@ int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
 /* persistent = 1 when the whole stack runs as one persistent launch, 0 for the
  * sequential form; launches = kernel launches of the last run (1 persistent). */
 int dsq_cuda_stack_info(const dsq_cuda_stack* stack, uint32_t* persistent, uint32_t* launches);
-/* one decode step from host buffers: copy x_host (x_bytes, pinned for async)
- * into x_dev (the stack's external input), run the stack, copy y_dev into
- * y_host, synchronise the stream.  A 0 byte count skips that copy. */
+/* one decode step from host buffers: copy x_host (x_bytes) into x_dev (the
+ * stack's external input), run the stack, copy y_dev into y_host, synchronise
+ * the stream.  A 0 byte count skips that copy.  Pinned (device-mapped) x_host
+ * with 16-byte aligned buffers and size is read by the GPU itself in a small
+ * upload kernel that the stack launch overlaps (programmatic dependent
+ * launch); other host memory goes through cudaMemcpyAsync. */
 int dsq_cuda_stack_run_host(dsq_cuda_stack* stack, const void* x_host, void* x_dev,
                             size_t x_bytes, const void* y_dev, void* y_host, size_t y_bytes,
                             void* stream);

@@ -31,6 +31,7 @@ cudaError_t launch_decode(int mode, const LayerParams& P, void* out, cudaStream_
 cudaError_t launch_f32_to_f16(const float* in, uint16_t* out, uint32_t n, cudaStream_t st,
                               bool pdl);
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl);
+cudaError_t launch_upload_x(const void* host, void* dev, size_t bytes, cudaStream_t st);
 cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut,
                          const uint32_t* row_ptr, const uint32_t* csr, uint32_t rows,
                          uint32_t cols, uint32_t ns, uint32_t tiles4, const uint16_t* x,
@@ -1335,7 +1336,20 @@ int dsq_cuda_stack_run_host(dsq_cuda_stack* S, const void* x_host, void* x_dev, 
         return fail(DSQ_E_INVALID_ARGUMENT, "stack_run_host: null buffer");
     cudaSetDevice(S->device);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (x_bytes) CUDA_TRY(cudaMemcpyAsync(x_dev, x_host, x_bytes, cudaMemcpyHostToDevice, st));
+    if (x_bytes) {
+        // pinned (device-mapped) host x, 16-byte multiple: the GPU reads it
+        // itself, overlapped with the stack kernel's prologue; else a memcpy
+        cudaPointerAttributes at{};
+        const bool mapped = cudaPointerGetAttributes(&at, x_host) == cudaSuccess &&
+                            at.type == cudaMemoryTypeHost && at.devicePointer == x_host &&
+                            !(reinterpret_cast<uintptr_t>(x_host) & 15u) &&
+                            !(reinterpret_cast<uintptr_t>(x_dev) & 15u) && x_bytes % 16 == 0;
+        cudaGetLastError();
+        if (mapped && !S->seq)
+            CUDA_TRY(launch_upload_x(x_host, x_dev, x_bytes, st));
+        else
+            CUDA_TRY(cudaMemcpyAsync(x_dev, x_host, x_bytes, cudaMemcpyHostToDevice, st));
+    }
     const int rc = dsq_cuda_stack_run(S, stream);
     if (rc) return rc;
     if (y_bytes) CUDA_TRY(cudaMemcpyAsync(y_host, y_dev, y_bytes, cudaMemcpyDeviceToHost, st));

@@ -494,6 +494,34 @@ cudaError_t launch_decode(int mode, const LayerParams& P, void* out, cudaStream_
     }
 }
 
+// host -> device copy of a step's input by the GPU itself (reads mapped pinned
+// host memory over PCIe).  It triggers its dependents at once, so the stack
+// kernel launched after it (PDL) runs its weight prologue -- ring loads, LUT
+// planes -- while the bytes cross the bus, and waits for them at its
+// griddepcontrol.wait; a copy-engine memcpy would serialise the two instead.
+__global__ void __launch_bounds__(256) upload_x(const uint4* __restrict__ src, uint4* dst,
+                                                uint32_t n16) {
+    pdl_trigger();
+    pdl_wait();  // dst may still be read by the previous launch on the stream
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t launch_upload_x(const void* host, void* dev, size_t bytes, cudaStream_t st) {
+    const uint32_t n16 = uint32_t(bytes / 16);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::max<uint32_t>(1, std::min<uint32_t>((n16 + 255) / 256, 16)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, upload_x, static_cast<const uint4*>(host),
+                              static_cast<uint4*>(dev), n16);
+}
+
 cudaError_t launch_f32_to_f16(const float* in, uint16_t* out, uint32_t n, cudaStream_t st,
                               bool pdl) {
     cudaLaunchConfig_t cfg = {};
