@@ -383,8 +383,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     src[:] = outs[CHAIN_IN[j]]
                 outs.append(dl.matvec_host(N.KERNEL_FUSED, src).astype(np.float32))
 
-        host_step(0)
-        nh = 10
+        nh = 20
+        for s in range(min(nh, n_rot)):  # every layer's host staging once
+            host_step(s)
         t0 = time.perf_counter()
         for s in range(nh):
             host_step(s % n_rot)

@@ -322,6 +322,10 @@ struct dsq_cuda_layer {
     uint16_t* x16 = nullptr;    // fp16 staging of an fp32 x
     float* y32 = nullptr;       // host-API output staging
     float* x32 = nullptr;       // host-API input staging
+    float* x32_pin = nullptr;   // host-API pinned, device-mapped staging (lazy)
+    float* y32_pin = nullptr;
+    float* x32_map = nullptr;   // their device addresses
+    float* y32_map = nullptr;
     uint16_t* dense_w = nullptr;  // lazily materialized fp16 dense W (reference kernel)
     // tile-record layout (bits 3/4): the persistent stack kernel's format
     bool rec_layout = false;
@@ -740,6 +744,8 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (!L) return DSQ_OK;
     cudaSetDevice(L->device);
     if (L->stream) cudaStreamDestroy(L->stream);
+    if (L->x32_pin) cudaFreeHost(L->x32_pin);
+    if (L->y32_pin) cudaFreeHost(L->y32_pin);
     if (L->dense_w) cudaFree(L->dense_w);
     if (L->batch_part) cudaFree(L->batch_part);
     if (L->gseg2) cudaFree(L->gseg2);
@@ -972,15 +978,31 @@ int dsq_cuda_matvec_host(const dsq_cuda_layer* Lc, int kernel, const float* x_ho
     if (!L || !x_host || !y_host) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     cudaSetDevice(L->device);
     std::lock_guard<std::mutex> lk(L->host_mu);
-    CUDA_TRY(cudaMemcpyAsync(L->x32, x_host, size_t(L->cols) * 4, cudaMemcpyHostToDevice,
-                             L->stream));
-    int rc = gemv_impl(L, kernel, L->x32, DSQ_F32, L->y32, DSQ_F32, 1, L->stream, false);
+    // pinned, device-mapped staging: the fp32 -> fp16 kernel reads x over
+    // PCIe and the product writes y straight into host memory, so a call is
+    // two launches (the second overlapping the first under PDL) and one
+    // synchronisation, no copy-engine transfers
+    if (!L->x32_pin) {
+        const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
+        cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&L->x32_pin), size_t(L->cols) * 4, fl);
+        if (e == cudaSuccess)
+            e = cudaHostAlloc(reinterpret_cast<void**>(&L->y32_pin), size_t(L->rows) * 4, fl);
+        if (e == cudaSuccess)
+            e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->x32_map), L->x32_pin, 0);
+        if (e == cudaSuccess)
+            e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->y32_map), L->y32_pin, 0);
+        if (e != cudaSuccess) {
+            if (L->x32_pin) cudaFreeHost(L->x32_pin);
+            if (L->y32_pin) cudaFreeHost(L->y32_pin);
+            L->x32_pin = L->y32_pin = L->x32_map = L->y32_map = nullptr;
+            return cuda_fail(e, "host-API staging");
+        }
+    }
+    std::memcpy(L->x32_pin, x_host, size_t(L->cols) * 4);
+    int rc = gemv_impl(L, kernel, L->x32_map, DSQ_F32, L->y32_map, DSQ_F32, 1, L->stream, true);
     if (rc) return rc;
-    std::vector<float> y(L->rows);
-    CUDA_TRY(cudaMemcpyAsync(y.data(), L->y32, size_t(L->rows) * 4, cudaMemcpyDeviceToHost,
-                             L->stream));
     CUDA_TRY(cudaStreamSynchronize(L->stream));
-    for (uint32_t r = 0; r < L->rows; ++r) y_host[r] = double(y[r]);
+    for (uint32_t r = 0; r < L->rows; ++r) y_host[r] = double(L->y32_pin[r]);
     return DSQ_OK;
 }
 
