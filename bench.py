@@ -362,14 +362,69 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": round(world * bytes_step * n_e2e / el / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": SHAPES[-1][1] * 2,
-               "steps": n_e2e, "ms_per_step": round(el / n_e2e * 1e3, 4),
-               "api": "DeviceStack.run_host (dsq_cuda_stack_run_host) per decoder-layer step: "
-                      "pinned host x -> device (read by a 1-CTA upload kernel whose PCIe latency "
-                      "overlaps the stack kernel's weight prologue under PDL), the 7-GEMV stack writing the step "
-                      "output straight into pinned host memory (zero-copy), stream synchronised "
-                      "every step"}
+        launch_form = {
+            "value": round(world * bytes_step * n_e2e / el / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(el / n_e2e * 1e3, 4),
+            "api": "DeviceStack.run_host (dsq_cuda_stack_run_host), one launch + one stream "
+                   "synchronisation per step: pinned host x read by a 1-CTA upload kernel "
+                   "overlapped with the stack kernel's prologue (PDL), the step output written "
+                   "straight into pinned host memory"}
+
+        # the serving loop (dsq_cuda_serve_*): the n_e2e steps as ONE resident
+        # launch fed step by step -- x_host -> x_dev on the copy engine, the
+        # step's doorbell behind it, the step's result (down projection) written
+        # by the kernel into pinned host memory and read into a numpy array
+        # once the kernel's completion word for the step arrives
+        y_all = torch.zeros(n_e2e * SHAPES[-1][1], dtype=torch.int16).pin_memory()
+        y_np = y_all.numpy()
+        y_out = np.empty(SHAPES[-1][1], dtype=np.int16)
+        layers, deps, xp, yp, gate, notify = [], [], [], [], [], []
+        for st_i in range(n_e2e):
+            slot, base = st_i % n_rot, len(layers)
+            for j, dl in enumerate(dls[slot]):
+                last = j == len(SHAPES) - 1
+                layers.append(dl)
+                deps.append(-1 if CHAIN_IN[j] < 0 else base + CHAIN_IN[j])
+                xp.append(x_dev.data_ptr() if CHAIN_IN[j] < 0 else 0)
+                gate.append(st_i + 1 if CHAIN_IN[j] < 0 else 0)
+                yp.append(y_all.data_ptr() + st_i * SHAPES[-1][1] * 2 if last
+                          else ys[slot][j].data_ptr())
+                notify.append(st_i + 1 if last else 0)
+        served = DeviceStack(layers, deps, xp, yp, N.F16, serve_gate=gate, serve_notify=notify)
+        torch.cuda.synchronize()
+        served.serve_begin(x_dev.data_ptr(), x_host.numel() * 2, sp)  # warm-up pass
+        for st_i in range(3):  # (the steps not fed are released by serve_end)
+            served.serve_step(x_host.data_ptr())
+        served.serve_end()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        served.serve_begin(x_dev.data_ptr(), x_host.numel() * 2, sp)
+        for st_i in range(n_e2e):
+            served.serve_step(x_host.data_ptr())
+            np.copyto(y_out, y_np[st_i * SHAPES[-1][1]:(st_i + 1) * SHAPES[-1][1]])
+        served.serve_end()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        serving = {
+            "value": round(world * bytes_step * n_e2e / el / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(el / n_e2e * 1e3, 4),
+            "api": "DeviceStack.serve_begin/serve_step/serve_end (dsq_cuda_stack_create_served, "
+                   "dsq_cuda_serve_*): the decode steps as one resident launch (inside the "
+                   "timed region) fed per step from host memory -- x copied into pinned "
+                   "staging + a doorbell word, CTA 0 of the kernel pulls the bytes over PCIe "
+                   "into the device x and releases the grid; the step output written by the "
+                   "kernel into pinned host memory and copied out after the kernel's "
+                   "completion word; no CUDA call, launch or stream synchronisation per step "
+                   "(tools/serve_trace.py: ~44 us of GPU work + ~14 us host round trip per step)"}
+        # the headline e2e is the faster of the two public per-step paths
+        e2e = dict(launch_form)
+        e2e.update({"h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": SHAPES[-1][1] * 2,
+                    "steps": n_e2e, "serving_loop": serving})
         # the reference-signature host call, per GEMV (fp32 host x -> fp64 host y,
         # dsq_cuda_matvec_host = fused_dns_matvec(layer, x)), for comparison
         xh = make_x(4096).astype(np.float32)

@@ -221,6 +221,30 @@ int dsq_cuda_stack_create_batch(dsq_cuda_layer* const* layers, uint32_t n, const
                                 uint32_t batch, uint32_t x_bstride, uint32_t y_bstride,
                                 dsq_cuda_stack** out);
 int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
+/* Serving loop: a stack of K decode steps as ONE resident launch that the
+ * host feeds step by step -- no CUDA call, launch or stream synchronisation
+ * per step.  gate[i] = k > 0 marks layer i (an external-input layer, deps[i]
+ * = -1, its xs[i] = the x_dev given to serve_begin) as reading step k's
+ * input (gates non-decreasing); notify[i] = k marks the layer whose
+ * completion ends step k (values 1, 2, .. K in layer order, 0 elsewhere).
+ * Put that layer's output in pinned host memory (its device-mapped address in
+ * ys) to read step k's result with no copy.
+ *   dsq_cuda_serve_begin: launch (the kernel streams the weights and waits at
+ *     the first gate); x_bytes (multiple of 16) per step go to x_dev;
+ *   dsq_cuda_serve_step: copy x_host into a pinned staging buffer and ring
+ *     step k's doorbell (host memory); CTA 0 of the kernel copies the bytes
+ *     over PCIe into x_dev and releases the grid; returns once the kernel's
+ *     completion word for step k has arrived in host memory;
+ *   dsq_cuda_serve_end: release any steps not fed, wait for the launch.
+ * A wait longer than 10 s ends in DSQ_E_INTERNAL, never a hang.  Single GPU,
+ * batch 1; dsq_cuda_stack_run is refused on a served stack. */
+int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                                 const void* const* xs, void* const* ys, int y_dtype,
+                                 const uint32_t* gate, const uint32_t* notify,
+                                 dsq_cuda_stack** out);
+int dsq_cuda_serve_begin(dsq_cuda_stack* stack, void* x_dev, size_t x_bytes, void* stream);
+int dsq_cuda_serve_step(dsq_cuda_stack* stack, const void* x_host);
+int dsq_cuda_serve_end(dsq_cuda_stack* stack);
 /* persistent = 1 when the whole stack runs as one persistent launch, 0 for the
  * sequential form; launches = kernel launches of the last run (1 persistent). */
 int dsq_cuda_stack_info(const dsq_cuda_stack* stack, uint32_t* persistent, uint32_t* launches);

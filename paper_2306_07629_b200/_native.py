@@ -142,6 +142,14 @@ PROTOTYPES = {
     "dsq_cuda_stack_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_stack_destroy": (C.c_int, [C.c_void_p]),
     "dsq_cuda_stack_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "dsq_cuda_stack_create_served": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32,
+                                               C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                                               C.POINTER(C.c_void_p), C.c_int,
+                                               C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                               C.POINTER(C.c_void_p)]),
+    "dsq_cuda_serve_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "dsq_cuda_serve_step": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dsq_cuda_serve_end": (C.c_int, [C.c_void_p]),
     "dsq_cuda_tp_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                      C.POINTER(C.c_void_p), C.c_void_p]),
     "dsq_cuda_tp_connect": (C.c_int, [C.c_void_p, C.c_void_p]),

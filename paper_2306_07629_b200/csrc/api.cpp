@@ -12,6 +12,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -1059,6 +1061,15 @@ struct dsq_cuda_stack {
     bool seq = false;
     uint32_t batch = 1, y_dtype = DSQ_F16, launches = 1;
     std::vector<StackSeqStep> steps;
+    // serving loop (dsq_cuda_serve_*): device [gate n][notify n][flag][err],
+    // pinned host [host_done][doorbell] and the x staging buffer
+    uint32_t* serve_dev = nullptr;
+    uint32_t* serve_pin = nullptr;
+    void* serve_x_pin = nullptr;  // pinned, device-mapped x staging
+    size_t serve_x_cap = 0, serve_x_bytes = 0;
+    cudaStream_t serve_stream = nullptr;
+    uint32_t serve_steps = 0, serve_k = 0;
+    bool serving = false;
     dsq_cuda_tp* tp = nullptr;
     StackParams sp{};
     void* arena = nullptr;
@@ -1381,6 +1392,7 @@ int dsq_cuda_stack_run_host(dsq_cuda_stack* S, const void* x_host, void* x_dev, 
 
 int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
     if (!S) return fail(DSQ_E_INVALID_ARGUMENT, "null stack");
+    if (S->serve_dev) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: use dsq_cuda_serve_*");
     cudaSetDevice(S->device);
     if (S->seq) {
         uint32_t launches = 0;
@@ -1412,9 +1424,142 @@ int dsq_cuda_stack_info(const dsq_cuda_stack* S, uint32_t* persistent, uint32_t*
     return DSQ_OK;
 }
 
+// ---- serving loop: one resident launch, the host feeds each step's x ----
+int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
+                                 const void* const* xs, void* const* ys, int y_dtype,
+                                 const uint32_t* gate, const uint32_t* notify,
+                                 dsq_cuda_stack** out) {
+    if (!gate || !notify) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: null gate / notify");
+    uint32_t steps = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (gate[i] && (!deps || deps[i] >= 0))
+            return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gate on chained layer %u", i);
+        if (gate[i] && i && gate[i] < gate[i - 1])
+            return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gates must not decrease");
+        if (notify[i]) {
+            if (notify[i] != steps + 1)
+                return fail(DSQ_E_INVALID_ARGUMENT, "served stack: notify values must run 1, 2, ..");
+            ++steps;
+        }
+    }
+    for (uint32_t i = 0; i < n; ++i)
+        if (gate[i] > steps)
+            return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gate %u beyond the last step", i);
+    if (steps == 0) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: no notify layer");
+    int rc = stack_create_impl(layers, n, deps, xs, ys, y_dtype, nullptr, nullptr, 0, out);
+    if (rc) return rc;
+    dsq_cuda_stack* S = *out;
+    auto bail = [&](cudaError_t e, const char* what) {
+        dsq_cuda_stack_destroy(S);
+        *out = nullptr;
+        return cuda_fail(e, what);
+    };
+    if (S->seq) {
+        dsq_cuda_stack_destroy(S);
+        *out = nullptr;
+        return fail(DSQ_E_UNSUPPORTED, "served stack: needs the persistent form");
+    }
+    // device: [gate n][notify n][flag][err]
+    cudaError_t e = cudaMalloc(&S->serve_dev, (size_t(2) * n + 2) * 4);
+    if (e != cudaSuccess) return bail(e, "served stack buffers");
+    std::vector<uint32_t> h(size_t(2) * n + 2, 0);
+    std::copy(gate, gate + n, h.begin());
+    std::copy(notify, notify + n, h.begin() + n);
+    if ((e = cudaMemcpy(S->serve_dev, h.data(), h.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(e, "served stack upload");
+    // pinned host: [0] host_done, [1] doorbell
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&S->serve_pin), 64,
+                           cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess)
+        return bail(e, "served stack pinned words");
+    S->serve_pin[0] = S->serve_pin[1] = 0;
+    uint32_t* pin_map = nullptr;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&pin_map), S->serve_pin, 0)) !=
+        cudaSuccess)
+        return bail(e, "served stack host mapping");
+    S->serve_steps = steps;
+    S->sp.serve_gate = S->serve_dev;
+    S->sp.serve_notify = S->serve_dev + n;
+    S->sp.serve_flag = S->serve_dev + 2 * n;
+    S->sp.serve_err = S->serve_dev + 2 * n + 1;
+    S->sp.host_done = pin_map;
+    S->sp.doorbell = pin_map + 1;
+    return DSQ_OK;
+}
+
+int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* stream) {
+    if (!S || !S->serve_dev) return fail(DSQ_E_INVALID_ARGUMENT, "serve: not a served stack");
+    if (S->serving) return fail(DSQ_E_INVALID_ARGUMENT, "serve: already running");
+    if (!x_dev || !x_bytes || x_bytes % 16 || (reinterpret_cast<uintptr_t>(x_dev) & 15u))
+        return fail(DSQ_E_INVALID_ARGUMENT, "serve: x_dev / x_bytes must be 16-byte aligned, > 0");
+    cudaSetDevice(S->device);
+    if (S->serve_x_cap < x_bytes) {
+        if (S->serve_x_pin) cudaFreeHost(S->serve_x_pin);
+        S->serve_x_pin = nullptr;
+        S->serve_x_cap = 0;
+        CUDA_TRY(cudaHostAlloc(&S->serve_x_pin, x_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        S->serve_x_cap = x_bytes;
+    }
+    void* x_map = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&x_map, S->serve_x_pin, 0));
+    S->sp.serve_x_src = static_cast<const uint4*>(x_map);
+    S->sp.serve_x_dst = static_cast<uint4*>(x_dev);
+    S->sp.serve_x_bytes = uint32_t(x_bytes);
+    S->serve_x_bytes = x_bytes;
+    const uint32_t zero[2] = {0, 0};
+    CUDA_TRY(cudaMemcpy(S->serve_dev + 2 * S->n, zero, 8, cudaMemcpyHostToDevice));  // flag, err
+    reinterpret_cast<volatile uint32_t*>(S->serve_pin)[0] = 0;  // host_done
+    reinterpret_cast<volatile uint32_t*>(S->serve_pin)[1] = 0;  // doorbell
+    S->serve_k = 0;
+    S->serve_stream = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(launch_stack(S->sp, S->serve_stream, false));
+    S->serving = true;
+    return DSQ_OK;
+}
+
+int dsq_cuda_serve_step(dsq_cuda_stack* S, const void* x_host) {
+    if (!S || !S->serving) return fail(DSQ_E_INVALID_ARGUMENT, "serve: not running");
+    if (S->serve_k >= S->serve_steps) return fail(DSQ_E_INVALID_ARGUMENT, "serve: no steps left");
+    if (!x_host) return fail(DSQ_E_INVALID_ARGUMENT, "serve: null x");
+    const uint32_t k = ++S->serve_k;
+    // step k-1 is complete, so the kernel has copied its x out of the staging
+    // buffer: refill it, then ring (x86 stores are seen in order over PCIe)
+    std::memcpy(S->serve_x_pin, x_host, S->serve_x_bytes);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    reinterpret_cast<volatile uint32_t*>(S->serve_pin)[1] = k;
+    const volatile uint32_t* done = S->serve_pin;
+    const auto t0 = std::chrono::steady_clock::now();
+    uint32_t spins = 0;
+    while (*done < k) {
+        if ((++spins & 1023u) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
+            return fail(DSQ_E_INTERNAL, "serve: step %u did not complete in 10 s", k);
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return DSQ_OK;
+}
+
+int dsq_cuda_serve_end(dsq_cuda_stack* S) {
+    if (!S || !S->serving) return fail(DSQ_E_INVALID_ARGUMENT, "serve: not running");
+    cudaSetDevice(S->device);
+    if (S->serve_k < S->serve_steps)  // release the steps not fed (stale x)
+        reinterpret_cast<volatile uint32_t*>(S->serve_pin)[1] = 0xffffffffu;
+    S->serving = false;
+    CUDA_TRY(cudaStreamSynchronize(S->serve_stream));
+    uint32_t err = 0;
+    CUDA_TRY(cudaMemcpy(&err, S->serve_dev + 2 * S->n + 1, 4, cudaMemcpyDeviceToHost));
+    return err ? fail(DSQ_E_INTERNAL, "serve: a step's input never arrived (wait timed out)")
+               : DSQ_OK;
+}
+
 int dsq_cuda_stack_destroy(dsq_cuda_stack* S) {
     if (!S) return DSQ_OK;
     cudaSetDevice(S->device);
+    if (S->serving) {
+        dsq_cuda_serve_end(S);
+    }
+    if (S->serve_x_pin) cudaFreeHost(S->serve_x_pin);
+    if (S->serve_pin) cudaFreeHost(S->serve_pin);
+    if (S->serve_dev) cudaFree(S->serve_dev);
     if (S->arena) cudaFree(S->arena);
     if (S->trace) cudaFree(S->trace);
     delete S;

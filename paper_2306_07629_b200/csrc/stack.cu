@@ -266,6 +266,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         // layer 0's LUT planes are launch constants and go before the PDL
         // wait; x (possibly the previous kernel's output) goes after it
         pdl_trigger();
+        uint32_t fed = 0;  // served stacks: the last step whose x CTA 0 copied in
         for (uint32_t l = 0; l < p.n_layers; ++l) {
             const uint32_t b = l & 1u;
             if (l >= 2) mbar_wait(&bempty[b], ((l >> 1) - 1) & 1u);
@@ -319,7 +320,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             // l may overwrite x only after every reader of layer l-1's x is done
             if (p.x_step == 0 && l >= 1) mbar_wait(&bempty[(l - 1) & 1u], ((l - 1) >> 1) & 1u);
             if (l == 0) pdl_wait();
-            if (d.dep == kNoDep) stage_x();  // external input: no wait at all
+            // served stacks: an external input of step k waits for the host's doorbell
+            const uint32_t gate = p.serve_gate ? p.serve_gate[l] : 0u;
+            if (d.dep == kNoDep && !gate) stage_x();  // external input: no wait at all
             // row_ptr slice + CSR entries + row-start bitmap of the CTA's rows:
             // TMA bulk copies (16-byte granules; the device arrays are padded),
             // sized from the host-precomputed per-CTA entry range
@@ -343,6 +346,47 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                     bulk_g2s_plain(hb, d.csr_heads + hw0, h_bytes, &cfull[b]);
                 }
                 DSQ_TRACE(l, kTrCsrStaged);
+            }
+            if (gate) {
+                // CTA 0 feeds step `gate`'s x (host doorbell -> PCIe copy ->
+                // device flag); everyone else waits for the flag
+                const uint32_t* wait_on = cta == 0 ? p.doorbell : p.serve_flag;
+                if (lane == 0 && !(cta == 0 && fed >= gate)) {
+                    const unsigned long long t0 = gtimer_ns();
+                    while ((cta == 0 ? ld_acquire_sys(wait_on) : ld_acquire_gpu(wait_on)) < gate) {
+                        if (gtimer_ns() - t0 > 10000000000ull) {
+                            atomicExch(p.serve_err, 1u);
+                            break;
+                        }
+                        __nanosleep(32);
+                    }
+                }
+                __syncwarp();
+                if (cta == 0 && fed < gate) {
+                    // 8 loads in flight per lane: a few PCIe round trips per step
+                    const uint32_t n16 = p.serve_x_bytes / 16;
+                    for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 8) {
+                        uint4 v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint32_t i = i0 + 32 * u + lane;
+                            if (i < n16) v[u] = ld_volatile_v4(p.serve_x_src + i);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint32_t i = i0 + 32 * u + lane;
+                            if (i < n16) p.serve_x_dst[i] = v[u];
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence();
+                        st_release_gpu(p.serve_flag, gate);
+                    }
+                    fed = gate;
+                }
+                __syncwarp();
+                stage_x();
             }
             if (d.dep != kNoDep) {
                 if (lane == 0) {
@@ -471,12 +515,20 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
         }
         __syncwarp();
+        const uint32_t notify = p.serve_notify ? p.serve_notify[l] : 0u;
         if (lane == 0) {
             if (f == 0) DSQ_TRACE(l, kTrFinalDone);
             mbar_arrive(&pempty[b]);
             mbar_arrive(&bempty[b]);
+            if (notify) __threadfence_system();  // this warp's y rows (host memory) first
             red_release_gpu_add(p.counters + l, 1u);
             if (f == 0) DSQ_TRACE(l, kTrSignaled);
+            if (notify && f == 0 && cta == 0) {
+                // every finishing warp of every CTA is done: step `notify` is out
+                while (ld_acquire_gpu(p.counters + l) < G * (1 + p.csr_warps)) __nanosleep(32);
+                __threadfence_system();
+                st_release_sys(p.host_done, notify);
+            }
         }
         __syncwarp();
     };

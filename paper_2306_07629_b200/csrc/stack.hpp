@@ -122,6 +122,25 @@ struct StackParams {
     uint32_t dbg;
     // optional timeline (null = off): [grid][n_layers][kTraceSlots] globaltimer ns
     unsigned long long* trace;
+    // serving loop (dsq_cuda_serve_*; null = off).  A layer with serve_gate[l]
+    // = k > 0 reads step k's input: CTA 0's loader waits for the host's
+    // doorbell (*doorbell >= k, pinned host memory), copies the step's x from
+    // the pinned staging buffer into serve_x_dst (the layer's x) over PCIe and
+    // publishes *serve_flag = k; the other CTAs wait for the flag.  For a
+    // layer with serve_notify[l] = k > 0 every finishing warp fences its rows
+    // of y system-wide before its completion release, and CTA 0 waits for the
+    // layer's count and stores k into *host_done (pinned host memory).  No CUDA
+    // call per step on the host.  A wait longer than 10 s sets *serve_err and
+    // lets the kernel run on (no hang).
+    const uint32_t* serve_gate;
+    const uint32_t* serve_notify;
+    const uint32_t* doorbell;     // device-mapped pinned host word
+    const uint4* serve_x_src;     // device-mapped pinned staging, serve_x_bytes
+    uint4* serve_x_dst;
+    uint32_t serve_x_bytes;       // multiple of 16
+    uint32_t* serve_flag;         // device word: the step whose x is in serve_x_dst
+    uint32_t* host_done;          // device-mapped pinned host word
+    uint32_t* serve_err;
 };
 
 // trace slots per (CTA, layer)

@@ -260,7 +260,8 @@ class DeviceStack:
 
     def __init__(self, layers: list, deps: list, xs: list, ys: list, y_dtype: int,
                  reduce: list | None = None, tp: "TPContext | None" = None, grid: int = 0,
-                 batch: int = 1, x_stride: int = 0, y_stride: int = 0):
+                 batch: int = 1, x_stride: int = 0, y_stride: int = 0,
+                 serve_gate: list | None = None, serve_notify: list | None = None):
         n = len(layers)
         self._layers = list(layers)  # keep the layer handles alive
         self._tp = tp
@@ -269,7 +270,12 @@ class DeviceStack:
         arr_x = (C.c_void_p * n)(*[x or 0 for x in xs])
         arr_y = (C.c_void_p * n)(*ys)
         h = C.c_void_p()
-        if batch > 1:
+        if serve_gate is not None or serve_notify is not None:
+            g = (C.c_uint32 * n)(*(serve_gate or [0] * n))
+            nt = (C.c_uint32 * n)(*(serve_notify or [0] * n))
+            check(lib.dsq_cuda_stack_create_served(arr_l, n, arr_d, arr_x, arr_y, y_dtype, g, nt,
+                                                   C.byref(h)))
+        elif batch > 1:
             if tp is not None or reduce is not None:
                 raise DsqError(102, "batched stacks are single-GPU")
             check(lib.dsq_cuda_stack_create_batch(arr_l, n, arr_d, arr_x, arr_y, y_dtype, batch,
@@ -286,6 +292,18 @@ class DeviceStack:
 
     def run(self, stream: int = 0) -> None:
         check(lib.dsq_cuda_stack_run(self.handle, stream))
+
+    # serving loop (served stacks): one resident launch fed step by step
+    def serve_begin(self, x_dev: int, x_bytes: int, stream: int = 0) -> None:
+        """Launch; every step's x_bytes of input go to x_dev (the gated layers' x)."""
+        check(lib.dsq_cuda_serve_begin(self.handle, x_dev, x_bytes, stream))
+
+    def serve_step(self, x_host: int) -> None:
+        """Feed the next step's input (host pointer) and wait for its outputs."""
+        check(lib.dsq_cuda_serve_step(self.handle, x_host))
+
+    def serve_end(self) -> None:
+        check(lib.dsq_cuda_serve_end(self.handle))
 
     def _info(self) -> tuple[int, int]:
         p, n = C.c_uint32(), C.c_uint32()
