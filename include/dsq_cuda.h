@@ -227,10 +227,11 @@ int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
  * = -1, its xs[i] = the x_dev given to serve_begin) as reading step k's
  * input (gates non-decreasing); notify[i] = k marks the layer whose
  * completion ends step k (values 1, 2, .. K in layer order, 0 elsewhere).
- * Put that layer's output in pinned host memory (its device-mapped address in
- * ys) to read step k's result with no copy.
  *   dsq_cuda_serve_begin: launch (the kernel streams the weights and waits at
- *     the first gate); x_bytes (multiple of 16) per step go to x_dev;
+ *     the first gate); x_bytes (multiple of 16) per step go to x_dev, and the
+ *     first y_bytes of each notify layer's output (device buffer, 16-byte
+ *     aligned) are copied by CTA 0 into y_host (pinned) before the step is
+ *     announced -- read them after dsq_cuda_serve_step returns;
  *   dsq_cuda_serve_step: copy x_host into a pinned staging buffer and ring
  *     step k's doorbell (host memory); CTA 0 of the kernel copies the bytes
  *     over PCIe into x_dev and releases the grid; returns once the kernel's
@@ -242,7 +243,8 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
                                  const void* const* xs, void* const* ys, int y_dtype,
                                  const uint32_t* gate, const uint32_t* notify,
                                  dsq_cuda_stack** out);
-int dsq_cuda_serve_begin(dsq_cuda_stack* stack, void* x_dev, size_t x_bytes, void* stream);
+int dsq_cuda_serve_begin(dsq_cuda_stack* stack, void* x_dev, size_t x_bytes, void* y_host,
+                         size_t y_bytes, void* stream);
 int dsq_cuda_serve_step(dsq_cuda_stack* stack, const void* x_host);
 int dsq_cuda_serve_end(dsq_cuda_stack* stack);
 /* persistent = 1 when the whole stack runs as one persistent launch, 0 for the

@@ -147,7 +147,8 @@ PROTOTYPES = {
                                                C.POINTER(C.c_void_p), C.c_int,
                                                C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                                C.POINTER(C.c_void_p)]),
-    "dsq_cuda_serve_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "dsq_cuda_serve_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                       C.c_size_t, C.c_void_p]),
     "dsq_cuda_serve_step": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_serve_end": (C.c_int, [C.c_void_p]),
     "dsq_cuda_tp_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,

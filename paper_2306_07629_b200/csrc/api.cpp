@@ -1067,6 +1067,7 @@ struct dsq_cuda_stack {
     uint32_t* serve_pin = nullptr;
     void* serve_x_pin = nullptr;  // pinned, device-mapped x staging
     size_t serve_x_cap = 0, serve_x_bytes = 0;
+    size_t serve_y_cap = 0;  // bytes of the smallest notify layer's y (0: unaligned)
     cudaStream_t serve_stream = nullptr;
     uint32_t serve_steps = 0, serve_k = 0;
     bool serving = false;
@@ -1446,6 +1447,12 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
         if (gate[i] > steps)
             return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gate %u beyond the last step", i);
     if (steps == 0) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: no notify layer");
+    size_t y_cap = SIZE_MAX;
+    for (uint32_t i = 0; i < n; ++i)
+        if (notify[i] && layers && layers[i] && ys && ys[i]) {
+            const size_t yb = size_t(layers[i]->rows) * (y_dtype == DSQ_F16 ? 2 : 4);
+            y_cap = (reinterpret_cast<uintptr_t>(ys[i]) & 15u) ? 0 : std::min(y_cap, yb);
+        }
     int rc = stack_create_impl(layers, n, deps, xs, ys, y_dtype, nullptr, nullptr, 0, out);
     if (rc) return rc;
     dsq_cuda_stack* S = *out;
@@ -1477,6 +1484,7 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
         cudaSuccess)
         return bail(e, "served stack host mapping");
     S->serve_steps = steps;
+    S->serve_y_cap = y_cap == SIZE_MAX ? 0 : y_cap;
     S->sp.serve_gate = S->serve_dev;
     S->sp.serve_notify = S->serve_dev + n;
     S->sp.serve_flag = S->serve_dev + 2 * n;
@@ -1486,12 +1494,26 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
     return DSQ_OK;
 }
 
-int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* stream) {
+int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* y_host,
+                         size_t y_bytes, void* stream) {
     if (!S || !S->serve_dev) return fail(DSQ_E_INVALID_ARGUMENT, "serve: not a served stack");
     if (S->serving) return fail(DSQ_E_INVALID_ARGUMENT, "serve: already running");
     if (!x_dev || !x_bytes || x_bytes % 16 || (reinterpret_cast<uintptr_t>(x_dev) & 15u))
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: x_dev / x_bytes must be 16-byte aligned, > 0");
+    if (y_bytes % 16 || (y_bytes && (!y_host || (reinterpret_cast<uintptr_t>(y_host) & 15u))))
+        return fail(DSQ_E_INVALID_ARGUMENT, "serve: y_host / y_bytes must be 16-byte aligned");
     cudaSetDevice(S->device);
+    S->sp.serve_y_dst = nullptr;
+    S->sp.serve_y_bytes = 0;
+    if (y_bytes) {
+        if (y_bytes > S->serve_y_cap)
+            return fail(DSQ_E_INVALID_ARGUMENT,
+                        "serve: y_bytes > a notify layer's output (or its y is not 16-byte aligned)");
+        void* y_map = nullptr;
+        CUDA_TRY(cudaHostGetDevicePointer(&y_map, y_host, 0));
+        S->sp.serve_y_dst = static_cast<uint4*>(y_map);
+        S->sp.serve_y_bytes = uint32_t(y_bytes);
+    }
     if (S->serve_x_cap < x_bytes) {
         if (S->serve_x_pin) cudaFreeHost(S->serve_x_pin);
         S->serve_x_pin = nullptr;

@@ -520,12 +520,32 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             if (f == 0) DSQ_TRACE(l, kTrFinalDone);
             mbar_arrive(&pempty[b]);
             mbar_arrive(&bempty[b]);
-            if (notify) __threadfence_system();  // this warp's y rows (host memory) first
             red_release_gpu_add(p.counters + l, 1u);
             if (f == 0) DSQ_TRACE(l, kTrSignaled);
-            if (notify && f == 0 && cta == 0) {
-                // every finishing warp of every CTA is done: step `notify` is out
+        }
+        if (notify && f == 0 && cta == 0) {
+            // every finishing warp of every CTA is done: copy step `notify`'s
+            // output to the host (one burst of PCIe writes), then announce it
+            if (lane == 0)
                 while (ld_acquire_gpu(p.counters + l) < G * (1 + p.csr_warps)) __nanosleep(32);
+            __syncwarp();
+            const uint32_t n16 = p.serve_y_bytes / 16;
+            const uint4* ysrc = static_cast<const uint4*>(d.y);
+            for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 8) {
+                uint4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t i = i0 + 32 * u + lane;
+                    if (i < n16) v[u] = ld_cg_v4(ysrc + i);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t i = i0 + 32 * u + lane;
+                    if (i < n16) p.serve_y_dst[i] = v[u];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
                 __threadfence_system();
                 st_release_sys(p.host_done, notify);
             }

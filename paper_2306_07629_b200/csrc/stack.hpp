@@ -129,7 +129,8 @@ struct StackParams {
     // publishes *serve_flag = k; the other CTAs wait for the flag.  For a
     // layer with serve_notify[l] = k > 0 every finishing warp fences its rows
     // of y system-wide before its completion release, and CTA 0 waits for the
-    // layer's count and stores k into *host_done (pinned host memory).  No CUDA
+    // layer's count, copies the layer's y (device memory) into serve_y_dst
+    // over PCIe and stores k into *host_done (pinned host memory).  No CUDA
     // call per step on the host.  A wait longer than 10 s sets *serve_err and
     // lets the kernel run on (no hang).
     const uint32_t* serve_gate;
@@ -139,6 +140,8 @@ struct StackParams {
     uint4* serve_x_dst;
     uint32_t serve_x_bytes;       // multiple of 16
     uint32_t* serve_flag;         // device word: the step whose x is in serve_x_dst
+    uint4* serve_y_dst;           // device-mapped pinned host: a notify layer's y copy
+    uint32_t serve_y_bytes;       // (0: none; multiple of 16)
     uint32_t* host_done;          // device-mapped pinned host word
     uint32_t* serve_err;
 };

@@ -294,9 +294,12 @@ class DeviceStack:
         check(lib.dsq_cuda_stack_run(self.handle, stream))
 
     # serving loop (served stacks): one resident launch fed step by step
-    def serve_begin(self, x_dev: int, x_bytes: int, stream: int = 0) -> None:
-        """Launch; every step's x_bytes of input go to x_dev (the gated layers' x)."""
-        check(lib.dsq_cuda_serve_begin(self.handle, x_dev, x_bytes, stream))
+    def serve_begin(self, x_dev: int, x_bytes: int, y_host: int = 0, y_bytes: int = 0,
+                    stream: int = 0) -> None:
+        """Launch; every step's x_bytes of input go to x_dev (the gated layers' x),
+        each step's output (notify layer, first y_bytes) to pinned y_host."""
+        check(lib.dsq_cuda_serve_begin(self.handle, x_dev, x_bytes, y_host or None, y_bytes,
+                                       stream))
 
     def serve_step(self, x_host: int) -> None:
         """Feed the next step's input (host pointer) and wait for its outputs."""

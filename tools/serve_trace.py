@@ -30,7 +30,7 @@ def main():
     x_dev = torch.zeros(4096, dtype=torch.int16, device="cuda")
     ys = [[torch.empty(r, dtype=torch.int16, device="cuda") for (_, r, _) in bench.SHAPES]
           for _ in range(rot)]
-    y_all = torch.zeros(K * 4096, dtype=torch.int16).pin_memory()
+    y_host = torch.zeros(4096, dtype=torch.int16).pin_memory()
     x_host = torch.from_numpy(make_x(4096, seed=7).view(np.int16)).pin_memory()
     layers, deps, xp, yp, gate, notify = [], [], [], [], [], []
     for k in range(K):
@@ -41,13 +41,13 @@ def main():
             deps.append(-1 if bench.CHAIN_IN[j] < 0 else base + bench.CHAIN_IN[j])
             xp.append(x_dev.data_ptr() if bench.CHAIN_IN[j] < 0 else 0)
             gate.append(k + 1 if bench.CHAIN_IN[j] < 0 else 0)
-            yp.append(y_all.data_ptr() + k * 8192 if last else ys[slot][j].data_ptr())
+            yp.append(ys[slot][j].data_ptr())
             notify.append(k + 1 if last else 0)
     st = DeviceStack(layers, deps, xp, yp, N.F16, serve_gate=gate, serve_notify=notify)
     torch.cuda.synchronize()
     host_us = []
     for rep in range(2):
-        st.serve_begin(x_dev.data_ptr(), 8192, 0)
+        st.serve_begin(x_dev.data_ptr(), 8192, y_host.data_ptr(), 8192, 0)
         for k in range(K):
             t0 = time.perf_counter()
             st.serve_step(x_host.data_ptr())
