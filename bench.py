@@ -420,11 +420,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "into the device x and releases the grid; CTA 0 copies the step output "
                    "into pinned host memory and writes the step's completion word, the host "
                    "copies it out; no CUDA call, launch or stream synchronisation per step "
-                   "(tools/serve_trace.py: ~44 us of GPU work + ~14 us host round trip per step)"}
+                   "(tools/serve_trace.py: ~37 us of GPU work + ~14 us host round trip per step)"}
         # the headline e2e is the faster of the two public per-step paths
-        e2e = dict(launch_form)
+        fast, other = (serving, launch_form) if serving["value"] >= launch_form["value"] \
+            else (launch_form, serving)
+        e2e = dict(fast)
         e2e.update({"h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": SHAPES[-1][1] * 2,
-                    "steps": n_e2e, "serving_loop": serving})
+                    "steps": n_e2e,
+                    ("per_step_launch" if other is launch_form else "serving_loop"): other})
         # the reference-signature host call, per GEMV (fp32 host x -> fp64 host y,
         # dsq_cuda_matvec_host = fused_dns_matvec(layer, x)), for comparison
         xh = make_x(4096).astype(np.float32)

@@ -187,7 +187,8 @@ __device__ __forceinline__ void csr_stream(uint32_t ea, uint32_t e0, uint32_t e1
     }
 }
 
-template <int BITS, int NC, int NB>
+// SERVE: the serving-loop variant (gates / notify, StackParams::serve_*)
+template <int BITS, int NC, int NB, bool SERVE = false>
 __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     stack_gemv(const __grid_constant__ StackParams p) {
     constexpr uint32_t LW = BITS == 3 ? 4u : 8u;   // LUT words per tile row
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             if (p.x_step == 0 && l >= 1) mbar_wait(&bempty[(l - 1) & 1u], ((l - 1) >> 1) & 1u);
             if (l == 0) pdl_wait();
             // served stacks: an external input of step k waits for the host's doorbell
-            const uint32_t gate = p.serve_gate ? p.serve_gate[l] : 0u;
+            const uint32_t gate = SERVE ? p.serve_gate[l] : 0u;
             if (d.dep == kNoDep && !gate) stage_x();  // external input: no wait at all
             // row_ptr slice + CSR entries + row-start bitmap of the CTA's rows:
             // TMA bulk copies (16-byte granules; the device arrays are padded),
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
         }
         __syncwarp();
-        const uint32_t notify = p.serve_notify ? p.serve_notify[l] : 0u;
+        const uint32_t notify = SERVE ? p.serve_notify[l] : 0u;
         if (lane == 0) {
             if (f == 0) DSQ_TRACE(l, kTrFinalDone);
             mbar_arrive(&pempty[b]);
@@ -909,21 +910,25 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static bool attr_done[14][64] = {};
+    static bool attr_done[18][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     const int ci = p.consumers == 8 ? 0 : 1;
     // nbatch 8 has only 8-consumer kernels (the accumulators of four vector
     // pairs need the registers)
-    const int bi = p.nbatch == 8 ? 12 + (p.bits == 3 ? 0 : 1)
+    if (p.serve_gate && p.nbatch != 1) return cudaErrorInvalidValue;  // served: batch 1
+    const int bi = p.serve_gate       ? 14 + (p.bits == 3 ? 0 : 1) * 2 + ci
+                   : p.nbatch == 8 ? 12 + (p.bits == 3 ? 0 : 1)
                                  : (p.nbatch == 4 ? 8 : p.nbatch == 2 ? 4 : 0) +
                                        (p.bits == 3 ? 0 : 1) * 2 + ci;
     using K = void (*)(StackParams);
-    static const K kerns[14] = {
+    static const K kerns[18] = {
         stack_gemv<3, 8, 1>, stack_gemv<3, 16, 1>, stack_gemv<4, 8, 1>, stack_gemv<4, 16, 1>,
         stack_gemv<3, 8, 2>, stack_gemv<3, 16, 2>, stack_gemv<4, 8, 2>, stack_gemv<4, 16, 2>,
         stack_gemv<3, 8, 4>, stack_gemv<3, 16, 4>, stack_gemv<4, 8, 4>, stack_gemv<4, 16, 4>,
-        stack_gemv<3, 8, 8>, stack_gemv<4, 8, 8>};
+        stack_gemv<3, 8, 8>, stack_gemv<4, 8, 8>,
+        stack_gemv<3, 8, 1, true>, stack_gemv<3, 16, 1, true>, stack_gemv<4, 8, 1, true>,
+        stack_gemv<4, 16, 1, true>};
     const K kern = kerns[bi];
     if (dev < 0 || dev >= 64 || !attr_done[bi][dev]) {
         int max_optin = 0;
