@@ -364,17 +364,17 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 }
                 __syncwarp();
                 if (cta == 0 && fed < gate) {
-                    // 8 loads in flight per lane: a few PCIe round trips per step
+                    // 16 loads in flight per lane: one PCIe round trip per 8 KB
                     const uint32_t n16 = p.serve_x_bytes / 16;
-                    for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 8) {
-                        uint4 v[8];
+                    for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 16) {
+                        uint4 v[16];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < 16; ++u) {
                             const uint32_t i = i0 + 32 * u + lane;
                             if (i < n16) v[u] = ld_volatile_v4(p.serve_x_src + i);
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < 16; ++u) {
                             const uint32_t i = i0 + 32 * u + lane;
                             if (i < n16) p.serve_x_dst[i] = v[u];
                         }
