@@ -1068,6 +1068,7 @@ struct dsq_cuda_stack {
     void* serve_x_pin = nullptr;  // pinned, device-mapped x staging
     size_t serve_x_cap = 0, serve_x_bytes = 0;
     size_t serve_y_cap = 0;  // bytes of the smallest notify layer's y (0: unaligned)
+    const void* serve_x_ptr = nullptr;  // the gated layers' (common) x buffer
     cudaStream_t serve_stream = nullptr;
     uint32_t serve_steps = 0, serve_k = 0;
     bool serving = false;
@@ -1447,6 +1448,13 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
         if (gate[i] > steps)
             return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gate %u beyond the last step", i);
     if (steps == 0) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: no notify layer");
+    const void* gx = nullptr;
+    for (uint32_t i = 0; i < n; ++i)
+        if (gate[i]) {
+            if (gx && xs && xs[i] != gx)
+                return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gated layers must share one x");
+            gx = xs ? xs[i] : nullptr;
+        }
     size_t y_cap = SIZE_MAX;
     for (uint32_t i = 0; i < n; ++i)
         if (notify[i] && layers && layers[i] && ys && ys[i]) {
@@ -1485,6 +1493,7 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
         return bail(e, "served stack host mapping");
     S->serve_steps = steps;
     S->serve_y_cap = y_cap == SIZE_MAX ? 0 : y_cap;
+    S->serve_x_ptr = gx;
     S->sp.serve_gate = S->serve_dev;
     S->sp.serve_notify = S->serve_dev + n;
     S->sp.serve_flag = S->serve_dev + 2 * n;
@@ -1500,6 +1509,8 @@ int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* y
     if (S->serving) return fail(DSQ_E_INVALID_ARGUMENT, "serve: already running");
     if (!x_dev || !x_bytes || x_bytes % 16 || (reinterpret_cast<uintptr_t>(x_dev) & 15u))
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: x_dev / x_bytes must be 16-byte aligned, > 0");
+    if (S->serve_x_ptr && x_dev != S->serve_x_ptr)
+        return fail(DSQ_E_INVALID_ARGUMENT, "serve: x_dev is not the gated layers' x buffer");
     if (y_bytes % 16 || (y_bytes && (!y_host || (reinterpret_cast<uintptr_t>(y_host) & 15u))))
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: y_host / y_bytes must be 16-byte aligned");
     cudaSetDevice(S->device);
