@@ -359,7 +359,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                             atomicExch(p.serve_err, 1u);
                             break;
                         }
-                        __nanosleep(32);
+                        if (cta != 0) __nanosleep(32);  // CTA 0's polls cross PCIe anyway
                     }
                 }
                 __syncwarp();
@@ -532,15 +532,15 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             __syncwarp();
             const uint32_t n16 = p.serve_y_bytes / 16;
             const uint4* ysrc = static_cast<const uint4*>(d.y);
-            for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 8) {
-                uint4 v[8];
+            for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 16) {
+                uint4 v[16];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 16; ++u) {
                     const uint32_t i = i0 + 32 * u + lane;
                     if (i < n16) v[u] = ld_cg_v4(ysrc + i);
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 16; ++u) {
                     const uint32_t i = i0 + 32 * u + lane;
                     if (i < n16) p.serve_y_dst[i] = v[u];
                 }
