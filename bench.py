@@ -44,11 +44,14 @@ METRIC = "LUT-GEMV µs/layer & effective HBM GB/s (% of peak); decode tok/s at 1
 # One decoder layer's GEMVs in dependency-aware issue order: v first so that o
 # (which consumes the attention output, stood in for by v's output) does not
 # wait; up before gate so that down (stand-in input: up's output) does not wait.
-SHAPES = [("v", 4096, 4096), ("q", 4096, 4096), ("k", 4096, 4096), ("o", 4096, 4096),
+# launch order of one decoder layer's GEMVs: o (<- v) is placed between q
+# and k so that k, which reads the step input, hides the o -> up/gate edge
+# and q hides the v -> o edge (the persistent kernel runs layers in order)
+SHAPES = [("v", 4096, 4096), ("q", 4096, 4096), ("o", 4096, 4096), ("k", 4096, 4096),
           ("up", 11008, 4096), ("gate", 11008, 4096), ("down", 4096, 11008)]
 # input of each GEMV (index into this step's outputs; -1 = the step input,
 # which is the previous step's down output -- steps chain like decoder layers)
-CHAIN_IN = [-1, -1, -1, 0, 3, 3, 4]
+CHAIN_IN = [-1, -1, 0, -1, 2, 2, 4]
 BITS, SPARSITY = 3, 0.0045
 LLAMA7B_LAYERS = 32
 
@@ -576,7 +579,8 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
         print(f"rank {rank}: tp watchdog: {e}", file=sys.stderr)
         ok = 0
     slot = (args.warmup - 1) % n_rot
-    sig = torch.stack([ys[slot][3].to(torch.int64).sum(), ys[slot][6].to(torch.int64).sum()])
+    o_i = [n for n, _, _ in SHAPES].index("o")
+    sig = torch.stack([ys[slot][o_i].to(torch.int64).sum(), ys[slot][6].to(torch.int64).sum()])
     sigs = [torch.zeros_like(sig) for _ in range(world)]
     dist.all_gather(sigs, sig)
     if any(not torch.equal(g, sigs[0]) for g in sigs):

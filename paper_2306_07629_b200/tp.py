@@ -101,9 +101,10 @@ def shard_cols(layer: QuantizedLayer, rank: int, world: int,
 # split of a producer equals the column split of its consumer (same 32-aligned
 # split_range), so o reads v's local slice and down reads up's local slice
 # with no exchange; the two reduces per decoder layer run inside the kernel.
-DECODER = ["v", "q", "k", "o", "up", "gate", "down"]
+# launch order (bench.py): o between q and k so that k hides the o -> up/gate edge
+DECODER = ["v", "q", "o", "k", "up", "gate", "down"]
 ROW_PARALLEL = {"o", "down"}
-CHAIN_IN = [-1, -1, -1, 0, 3, 3, 4]  # input of each GEMV within a step (bench.py)
+CHAIN_IN = [-1, -1, 0, -1, 2, 2, 4]  # input of each GEMV within a step (bench.py)
 
 
 def shard_decoder(layers: list, rank: int, world: int, align: int = 32) -> list:

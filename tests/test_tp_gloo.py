@@ -129,15 +129,18 @@ def test_decoder_shards_chain_locally():
            for i, n in enumerate(DECODER)]
     for world in (2, 4, 8):
         rows_v, rows_up, cols_o, cols_down = 0, 0, 0, 0
+        ix = {n: i for i, n in enumerate(DECODER)}
+        v, o, up, down = ix["v"], ix["o"], ix["up"], ix["down"]
         for r in range(world):
             s = shard_decoder(qls, r, world)
-            assert s[3].cols == s[0].rows and s[6].cols == s[4].rows
-            rows_v += s[0].rows
-            rows_up += s[4].rows
-            cols_o += s[3].cols
-            cols_down += s[6].cols
-            assert s[3].rows == 256 and s[6].rows == 256  # row-parallel: full outputs
+            assert s[o].cols == s[v].rows and s[down].cols == s[up].rows
+            rows_v += s[v].rows
+            rows_up += s[up].rows
+            cols_o += s[o].cols
+            cols_down += s[down].cols
+            assert s[o].rows == 256 and s[down].rows == 256  # row-parallel: full outputs
         assert rows_v == cols_o == 256 and rows_up == cols_down == 704
     deps, reduce, _ = decoder_chain(2, 1)
-    assert deps[:7] == [-1, -1, -1, 0, 3, 3, 4] and deps[7:10] == [6, 6, 6]
-    assert [i for i, r in enumerate(reduce) if r] == [3, 6, 10, 13]
+    assert deps[:7] == [-1, -1, 0, -1, 2, 2, 4] and deps[7:14] == [6, 6, 7, 6, 9, 9, 11]
+    assert [reduce[i] for i in range(7)] == [n in ("o", "down") for n in DECODER]
+    assert [i for i, r in enumerate(reduce) if r] == [2, 6, 9, 13]

@@ -40,7 +40,8 @@ CHAIN_IN = [-1, -1, -1, 0, 3, 3, 4]  # v,q,k,o,up,gate,down (bench.py)
 
 
 def shapes(h, f):
-    return [("v", h, h), ("q", h, h), ("k", h, h), ("o", h, h), ("up", f, h), ("gate", f, h),
+    # the decoder launch order of paper_2306_07629_b200.tp.DECODER
+    return [("v", h, h), ("q", h, h), ("o", h, h), ("k", h, h), ("up", f, h), ("gate", f, h),
             ("down", h, f)]
 
 
