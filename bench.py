@@ -423,7 +423,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "into the device x and releases the grid; CTA 0 copies the step output "
                    "into pinned host memory and writes the step's completion word, the host "
                    "copies it out; no CUDA call, launch or stream synchronisation per step "
-                   "(tools/serve_trace.py: ~37 us of GPU work + ~12 us host round trip per step)"}
+                   "(tools/serve_trace.py: ~34 us of GPU work + ~12 us host round trip per step)"}
         # the headline e2e is the faster of the two public per-step paths
         fast, other = (serving, launch_form) if serving["value"] >= launch_form["value"] \
             else (launch_form, serving)
