@@ -81,3 +81,11 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean cxx-test profile-lib watchdog-lib
+
+# dev: A/B variants of the stack kernel (DSQ_CUDA_LIB=<lib> selects one)
+# make variant-lib VNAME=foo VFLAGS="-DFOO" -> paper_2306_07629_b200/libdsq_cuda_foo.so
+VNAME ?= var
+VFLAGS ?=
+variant-lib: $(OBJS)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(CSRC)/stack.cu -o $(CSRC)/stack_$(VNAME).o 2> /dev/null
+	$(NVCC) $(ARCH) -shared -o $(PKG)/libdsq_cuda_$(VNAME).so $(filter-out $(CSRC)/stack.o,$(OBJS)) $(CSRC)/stack_$(VNAME).o -Xcompiler -fopenmp -lgomp

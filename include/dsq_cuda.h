@@ -170,6 +170,26 @@ int dsq_cuda_dense_gemv(const uint16_t* w_f16, uint32_t rows, uint32_t cols, con
 int dsq_cuda_matvec_host(const dsq_cuda_layer* layer, int kernel, const float* x_host,
                          double* y_host);
 
+/* ---- one-shot host products of the reference's free functions -------------
+ * (the C++ drop-ins sqz::lut_matvec / csr_matvec / dense_matvec /
+ * dequantize_layer in dsq_cuda.hpp call these; fp32 host x -> fp64 host y)
+ *   dsq_cuda_packed_matvec_host -> dsq::lut_matvec(PackedDense, x)  kernels.hpp:20
+ *   dsq_cuda_csr_matvec_host    -> dsq::csr_matvec(CsrMatrix, x)    kernels.hpp:24
+ *   dsq_cuda_dense_matvec_host  -> dsq::dense_matvec(m, rows, cols, x) kernels.hpp:35
+ *     (fp32 weights, fp64 accumulation of the exact fp32 products)
+ *   dsq_cuda_dequantize_layer   -> dsq::dequantize_layer(layer)     pipeline.cpp:49-75
+ *     w[rows*cols] fp32 = LUT value, and lut_row[0] + delta (one fp32 add)
+ *     at every CSR position; bit-equal to the reference for fp16-exact
+ *     LUTs/deltas (dsq_layer_info.luts_exact_f16 / values_exact_f16). */
+int dsq_cuda_packed_matvec_host(const dsq_packed_view* packed, const float* x_host,
+                                double* y_host, int device);
+int dsq_cuda_csr_matvec_host(const dsq_csr_view* sparse, const float* x_host, double* y_host,
+                             int device);
+int dsq_cuda_dense_matvec_host(const float* m_host, uint32_t rows, uint32_t cols,
+                               const float* x_host, double* y_host, int device);
+int dsq_cuda_dequantize_layer(const dsq_cuda_layer* layer, float* w_dev, void* stream);
+int dsq_cuda_dequantize_layer_host(const dsq_cuda_layer* layer, float* w_host);
+
 /* ---- debug / parity kernels ----------------------------------------------- */
 /* K5: device decode of the re-tiled index layout into the reference
  * AssignmentVector order (unpack, packfmt.cpp:57-80): assign[rows*cols] u16 */
@@ -177,6 +197,12 @@ int dsq_cuda_unpack(const dsq_cuda_layer* layer, uint16_t* assign_dev, void* str
 /* K6: device dequantization (ref::dequant_dense, kernels.cpp:149-159):
  * w[rows*cols] as fp16 bit patterns (out_dtype F16) or fp32 (F32) */
 int dsq_cuda_dequant(const dsq_cuda_layer* layer, void* w_dev, int out_dtype, void* stream);
+/* The fp16 A fragments of the hot product kernels (the same PRMT byte-plane
+ * decode the stack kernel times, stack.cu dump_frags) scattered back to a
+ * dense w[rows*cols] of fp16 bit patterns: equal, bit for bit, to
+ * ref::dequant_dense (kernels.cpp:149-159).  3/4-bit layers only
+ * (DSQ_E_UNSUPPORTED otherwise). */
+int dsq_cuda_dump_frags(const dsq_cuda_layer* layer, uint16_t* w_dev, void* stream);
 
 /* ---- accounting --------------------------------------------------------- */
 /* bytes_touched_estimate (kernels.cpp:205-212): the algorithmic bytes of one
@@ -237,8 +263,14 @@ int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
  *     over PCIe into x_dev and releases the grid; returns once the kernel's
  *     completion word for step k has arrived in host memory;
  *   dsq_cuda_serve_end: release any steps not fed, wait for the launch.
- * A wait longer than 10 s ends in DSQ_E_INTERNAL, never a hang.  Single GPU,
- * batch 1; dsq_cuda_stack_run is refused on a served stack. */
+ * Gated layers of step k must sit after notify k-1 and before notify k
+ * (gate[i] == 1 + the notify layers before i) and share one x buffer of
+ * their common cols; x_bytes must be cols*2 rounded up to at most 16.  The
+ * kernel waits for a step's doorbell without a timeout (an idle server may
+ * wait any time; it never computes on a stale x); dsq_cuda_serve_step gives
+ * up with DSQ_E_INTERNAL after 10 s without the step's completion word, and
+ * dsq_cuda_serve_end releases the steps not fed.  Single GPU, batch 1;
+ * dsq_cuda_stack_run is refused on a served stack. */
 int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
                                  const void* const* xs, void* const* ys, int y_dtype,
                                  const uint32_t* gate, const uint32_t* notify,

@@ -12,12 +12,16 @@
 //   sqz::DeviceLayer dev(layer);                  // validate + re-tile + upload once
 //   std::vector<double> y = dev.fused(x);          // == dsq::fused_dns_matvec(layer, x)
 //   std::vector<double> y2 = sqz::fused_dns_matvec(layer, x);   // one-shot form
+//   (also sqz::lut_matvec / csr_matvec / dense_matvec / bench_matvec /
+//    bytes_touched_estimate / dequantize_layer with the dsq:: signatures)
 //
 // Errors: a non-OK status is rethrown as sqz::Error whose errc() is the
 // reference's dsq::errc value (status - 1), so `static_cast<dsq::errc>(e.errc())`
 // reproduces dsq::Error and the CLI exit-code mapping (tools/dsq.cpp:399-411).
 #pragma once
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -122,19 +126,135 @@ private:
     size_t cols_ = 0, rows_ = 0;
 };
 
-// One-shot forms (upload + product; keep a DeviceLayer for repeated calls).
-template <class Layer>
-std::vector<double> fused_dns_matvec(const Layer& l, const std::vector<float>& x) {
-    return DeviceLayer(l).fused(x);
-}
-template <class Layer>
-std::vector<double> csr_part_matvec(const Layer& l, const std::vector<float>& x) {
-    return DeviceLayer(l).csr(x);
+// ---- the reference's free functions (kernels.hpp:20-79, pipeline.hpp) ------
+//
+// Same names, argument order and meaning as dsq::, so a reference caller
+// switches namespaces: `sqz::fused_dns_matvec(layer, x)`.  The Exec argument
+// is accepted as dsq::Exec or sqz::Exec; every value runs on the GPU (the
+// device products are deterministic whatever the launch configuration, the
+// guarantee dsq::Exec::parallel gives on the host, kernels.hpp:13-16).  The
+// one-shot forms upload the layer per call; keep a DeviceLayer for repeated
+// products.  Errors are rethrown as sqz::Error with the reference errc.
+enum class Exec { serial, parallel, cuda };
+
+// dsq::lut_matvec(const PackedDense&, const ActivationVector&, Exec)
+template <class Packed, class E = Exec>
+std::vector<double> lut_matvec(const Packed& p, const std::vector<float>& x, E = E{}) {
+    if (x.size() != p.cols) throw Error(DSQ_E_SHAPE_MISMATCH, "lut_matvec: dimension mismatch");
+    const dsq_packed_view v = packed_view(p);
+    std::vector<double> y(p.rows);
+    check(dsq_cuda_packed_matvec_host(&v, x.data(), y.data(), 0));
+    return y;
 }
 
+// dsq::csr_matvec(const CsrMatrix&, const ActivationVector&, Exec)
+template <class Csr, class E = Exec>
+std::vector<double> csr_matvec(const Csr& s, const std::vector<float>& x, E = E{}) {
+    if (x.size() != s.cols) throw Error(DSQ_E_SHAPE_MISMATCH, "csr_matvec: dimension mismatch");
+    const dsq_csr_view v = csr_view(s);
+    std::vector<double> y(s.rows);
+    check(dsq_cuda_csr_matvec_host(&v, x.data(), y.data(), 0));
+    return y;
+}
+
+// dsq::fused_dns_matvec(const QuantizedLayer&, const ActivationVector&, Exec)
+template <class Layer, class E = Exec>
+std::vector<double> fused_dns_matvec(const Layer& l, const std::vector<float>& x, E = E{}) {
+    return DeviceLayer(l).fused(x);
+}
+
+// dsq::dense_matvec(const std::vector<float>& m, rows, cols, x, Exec)
+template <class E = Exec>
+std::vector<double> dense_matvec(const std::vector<float>& m, uint32_t rows, uint32_t cols,
+                                 const std::vector<float>& x, E = E{}) {
+    if (m.size() != size_t(rows) * cols || x.size() != cols)
+        throw Error(DSQ_E_SHAPE_MISMATCH, "dense_matvec: dimension mismatch");
+    std::vector<double> y(rows);
+    check(dsq_cuda_dense_matvec_host(m.data(), rows, cols, x.data(), y.data(), 0));
+    return y;
+}
+
+// dsq::bytes_touched_estimate(const QuantizedLayer&) (kernels.cpp:205-212)
+template <class Layer>
+uint64_t bytes_touched_estimate(const Layer& l) {
+    const uint32_t gpr = l.packed.groups_per_row;
+    return dsq_bytes_touched_estimate(l.rows, l.cols, l.packed.bits, gpr == 1 ? 0 : l.cols / gpr,
+                                      l.sparse.row_ptr.empty() ? 0 : l.sparse.row_ptr.back());
+}
 inline uint64_t bytes_touched_estimate(uint32_t rows, uint32_t cols, uint32_t bits,
                                        uint32_t group_size, uint64_t nnz) {
     return dsq_bytes_touched_estimate(rows, cols, bits, group_size, nnz);
+}
+
+// dsq::BenchRecord / BenchKernel / bench_matvec (kernels.hpp:63-75,
+// kernels.cpp:214-282): median wall time of `repeats` (>= 3) products after
+// one warm-up, each timed around the reference-signature host call (fp32
+// host x -> fp64 host y on the uploaded layer), and the reference's per-kernel
+// byte charge.  The kernel argument may be dsq::BenchKernel or sqz::BenchKernel
+// (same order: lut, csr, fused, reference).
+struct BenchRecord {
+    std::string kernel;
+    uint32_t repeats = 0;
+    double median_seconds = 0.0;
+    std::vector<double> all_seconds;
+    uint64_t bytes_touched = 0;
+};
+enum class BenchKernel { lut, csr, fused, reference };
+
+template <class Layer, class K, class E = Exec>
+BenchRecord bench_matvec(const Layer& l, const std::vector<float>& x, uint32_t repeats, K kernel,
+                         E = E{}) {
+    if (repeats < 3) throw Error(DSQ_E_INVALID_ARGUMENT, "bench: repeats must be >= 3");
+    const int k = static_cast<int>(kernel);  // DSQ_KERNEL_LUT..REFERENCE
+    static const char* names[] = {"lut", "csr", "fused", "reference"};
+    if (k < 0 || k > 3) throw Error(DSQ_E_INVALID_ARGUMENT, "bench: unknown kernel");
+    DeviceLayer dev(l);
+    auto run = [&]() {
+        switch (k) {
+            case 0: return dev.lut(x);
+            case 1: return dev.csr(x);
+            case 2: return dev.fused(x);
+            default: return dev.reference(x);
+        }
+    };
+    (void)run();  // warm-up
+    BenchRecord rec;
+    rec.kernel = names[k];
+    rec.repeats = repeats;
+    for (uint32_t i = 0; i < repeats; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        (void)run();
+        const auto t1 = std::chrono::steady_clock::now();
+        rec.all_seconds.push_back(std::chrono::duration<double>(t1 - t0).count());
+    }
+    std::vector<double> s = rec.all_seconds;
+    std::sort(s.begin(), s.end());
+    rec.median_seconds = repeats % 2 ? s[repeats / 2] : 0.5 * (s[repeats / 2 - 1] + s[repeats / 2]);
+    const uint32_t gpr = l.packed.groups_per_row;
+    const uint32_t gs = gpr == 1 ? 0 : l.cols / gpr;
+    const uint64_t io = uint64_t(l.cols) * 2 + uint64_t(l.rows) * 2;
+    const uint64_t nnz = l.sparse.row_ptr.empty() ? 0 : l.sparse.row_ptr.back();
+    switch (k) {
+        case 0: rec.bytes_touched = dsq_bytes_touched_estimate(l.rows, l.cols, l.packed.bits, gs, 0); break;
+        case 1: rec.bytes_touched = nnz * 4 + (uint64_t(l.rows) + 1) * 4 + io; break;
+        case 2: rec.bytes_touched = bytes_touched_estimate(l); break;
+        default: rec.bytes_touched = uint64_t(l.rows) * l.cols * 2 + io; break;
+    }
+    return rec;
+}
+
+// dsq::dequantize_layer(const QuantizedLayer&) -> WeightMatrix (pipeline.cpp:49-75);
+// Matrix = dsq::WeightMatrix (name, rows, cols, values)
+template <class Matrix, class Layer>
+Matrix dequantize_layer(const Layer& l, int device = 0) {
+    DeviceLayer dev(l, device);
+    Matrix m;
+    m.name = l.name;
+    m.rows = l.rows;
+    m.cols = l.cols;
+    m.values.resize(size_t(l.rows) * l.cols);
+    check(dsq_cuda_dequantize_layer_host(dev.get(), m.values.data()));
+    return m;
 }
 
 // ---- the producer side on the GPU, with the caller's reference types ------

@@ -131,6 +131,13 @@ PROTOTYPES = {
     "dsq_cuda_matvec_host": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "dsq_cuda_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsq_cuda_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "dsq_cuda_dump_frags": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsq_cuda_dense_matvec_host": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                             C.c_void_p, C.c_int]),
+    "dsq_cuda_dequantize_layer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsq_cuda_dequantize_layer_host": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dsq_cuda_packed_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    "dsq_cuda_csr_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "dsq_bytes_touched_estimate": (C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                                 C.c_uint64]),
     "dsq_cuda_gemv_many": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.c_int,

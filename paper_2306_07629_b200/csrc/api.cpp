@@ -40,6 +40,14 @@ cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut
                          uint32_t x_stride, uint32_t B, void* y, uint32_t y_stride, bool y_f16,
                          float* part, uint32_t kslices, uint32_t spans_per_slice, int mode,
                          cudaStream_t st);
+cudaError_t launch_apply_deltas(const uint32_t* row_ptr, const uint32_t* csr, const uint16_t* lut,
+                                uint32_t K, uint32_t rows, uint32_t cols, float* w,
+                                cudaStream_t st);
+cudaError_t launch_dense_f32(const float* w, uint32_t rows, uint32_t cols, const float* x,
+                             double* y, int num_sms, cudaStream_t st);
+cudaError_t launch_dump_frags(uint32_t bits, const uint32_t* idx, const uint32_t* lut,
+                              uint32_t rows, uint32_t cols, uint32_t tiles, uint32_t ns,
+                              uint16_t* out, cudaStream_t st);
 cudaError_t launch_decode_tiles(int mode, uint32_t bits, const uint32_t* idx, const uint32_t* lut,
                                 uint32_t rows, uint32_t cols, uint32_t ns, void* out,
                                 cudaStream_t st);
@@ -299,6 +307,10 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.smem_bytes = sp.off_ring + sp.n_slots * sp.slot_bytes;
     sp.grid = uint32_t(G);
     sp.bits = bits;
+    sp.k29 = 1u << 29;
+    sp.k30 = 1u << 30;
+    sp.k31 = 1u << 31;
+    sp.kneg = 0xffffffffu;
     for (uint32_t i = 0; i < n && i < kInlineLayers; ++i)
         fill_desc(sp.inl[i], Ls[i], sp.slot_bytes, bits, G);
     return DSQ_OK;
@@ -1033,6 +1045,127 @@ int dsq_cuda_dequant(const dsq_cuda_layer* L, void* w_dev, int out_dtype, void* 
     return DSQ_OK;
 }
 
+int dsq_cuda_dump_frags(const dsq_cuda_layer* L, uint16_t* w_dev, void* stream) {
+    if (!L || !w_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (!L->rec_layout)
+        return fail(DSQ_E_UNSUPPORTED, "dump_frags: only the 3/4-bit tile layout has HMMA fragments");
+    cudaSetDevice(L->device);
+    CUDA_TRY(launch_dump_frags(L->bits, L->rec, L->tlut, L->rows, L->cols, L->tiles, L->ns, w_dev,
+                               static_cast<cudaStream_t>(stream)));
+    return DSQ_OK;
+}
+
+// ---- reference-signature host products (the sqz:: C++ drop-in functions) ----
+
+int dsq_cuda_dequantize_layer(const dsq_cuda_layer* L, float* w_dev, void* stream) {
+    if (!L || !w_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(L->device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (L->rec_layout)
+        CUDA_TRY(launch_decode_tiles(2, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns, w_dev,
+                                     st));
+    else
+        CUDA_TRY(launch_decode(2, L->P, w_dev, st));
+    if (L->nnz)
+        CUDA_TRY(launch_apply_deltas(L->P.row_ptr, L->P.csr, L->P.lut, 1u << L->bits, L->rows,
+                                     L->cols, w_dev, st));
+    return DSQ_OK;
+}
+
+int dsq_cuda_dequantize_layer_host(const dsq_cuda_layer* Lc, float* w_host) {
+    auto* L = const_cast<dsq_cuda_layer*>(Lc);
+    if (!L || !w_host) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(L->device);
+    std::lock_guard<std::mutex> lk(L->host_mu);
+    const size_t bytes = size_t(L->rows) * L->cols * 4;
+    float* w = nullptr;
+    CUDA_TRY(cudaMalloc(&w, bytes));
+    int rc = dsq_cuda_dequantize_layer(L, w, L->stream);
+    cudaError_t e = rc ? cudaSuccess : cudaMemcpyAsync(w_host, w, bytes, cudaMemcpyDeviceToHost,
+                                                       L->stream);
+    if (!rc && e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
+    cudaFree(w);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "dequantize_layer");
+    return DSQ_OK;
+}
+
+int dsq_cuda_dense_matvec_host(const float* m, uint32_t rows, uint32_t cols, const float* x,
+                               double* y, int device) {
+    if (!m || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (rows < 1 || cols < 1) return fail(DSQ_E_EMPTY_DIMENSION, "dense: empty dims");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(DSQ_E_NO_DEVICE, "no CUDA device visible");
+    if (device < 0 || device >= ndev) return fail(DSQ_E_NO_DEVICE, "bad device %d", device);
+    CUDA_TRY(cudaSetDevice(device));
+    int sms = 0;
+    int rc = query_num_sms(device, &sms);
+    if (rc) return rc;
+    const size_t wb = size_t(rows) * cols * 4;
+    uint8_t* buf = nullptr;
+    CUDA_TRY(cudaMalloc(&buf, wb + size_t(cols) * 4 + size_t(rows) * 8 + 512));
+    float* dw = reinterpret_cast<float*>(buf);
+    float* dx = reinterpret_cast<float*>(buf + ((wb + 255) & ~size_t(255)));
+    double* dy = reinterpret_cast<double*>(buf + ((wb + 255) & ~size_t(255)) +
+                                           ((size_t(cols) * 4 + 255) & ~size_t(255)));
+    cudaError_t e = cudaMemcpy(dw, m, wb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dx, x, size_t(cols) * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_dense_f32(dw, rows, cols, dx, dy, sms, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(y, dy, size_t(rows) * 8, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return cuda_fail(e, "dense_matvec");
+    return DSQ_OK;
+}
+
+// one-shot products of a bare PackedDense / CsrMatrix: a transient layer
+// whose other part is empty (no CSR entries / an all-zero 1-bit LUT part)
+int dsq_cuda_packed_matvec_host(const dsq_packed_view* p, const float* x, double* y,
+                                int device) {
+    if (!p || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    std::vector<uint32_t> zrp(size_t(p->rows) + 1, 0);
+    dsq_layer_view v{};
+    v.name = "packed";
+    v.rows = p->rows;
+    v.cols = p->cols;
+    v.packed = *p;
+    v.sparse.rows = p->rows;
+    v.sparse.cols = p->cols;
+    v.sparse.row_ptr = zrp.data();
+    dsq_cuda_layer* L = nullptr;
+    int rc = dsq_cuda_layer_create(&v, device, &L);
+    if (rc) return rc;
+    rc = dsq_cuda_matvec_host(L, DSQ_KERNEL_LUT, x, y);
+    dsq_cuda_layer_destroy(L);
+    return rc;
+}
+
+int dsq_cuda_csr_matvec_host(const dsq_csr_view* s, const float* x, double* y, int device) {
+    if (!s || !x || !y) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (s->cols >= 65536u) return fail(DSQ_E_DIMENSION_OVERFLOW, "csr: cols must be < 65536");
+    if (s->rows < 1 || s->cols < 1) return fail(DSQ_E_EMPTY_DIMENSION, "csr: empty dims");
+    std::vector<float> zl(size_t(s->rows) * 2, 0.f);
+    std::vector<uint8_t> zp(size_t(s->rows) * row_stride(s->cols, 1), 0);
+    dsq_layer_view v{};
+    v.name = "csr";
+    v.rows = s->rows;
+    v.cols = s->cols;
+    v.packed.bits = 1;
+    v.packed.rows = s->rows;
+    v.packed.cols = s->cols;
+    v.packed.groups_per_row = 1;
+    v.packed.luts_f32 = zl.data();
+    v.packed.payload = zp.data();
+    v.packed.payload_len = zp.size();
+    v.sparse = *s;
+    dsq_cuda_layer* L = nullptr;
+    int rc = dsq_cuda_layer_create(&v, device, &L);
+    if (rc) return rc;
+    rc = dsq_cuda_matvec_host(L, DSQ_KERNEL_CSR, x, y);
+    dsq_cuda_layer_destroy(L);
+    return rc;
+}
+
 struct dsq_cuda_tp {
     int device = 0;
     uint32_t world = 1, rank = 0, max_rows = 0, max_grid = 0;
@@ -1069,6 +1202,7 @@ struct dsq_cuda_stack {
     size_t serve_x_cap = 0, serve_x_bytes = 0;
     size_t serve_y_cap = 0;  // bytes of the smallest notify layer's y (0: unaligned)
     const void* serve_x_ptr = nullptr;  // the gated layers' (common) x buffer
+    uint32_t serve_x_cols = 0;          // their (common) column count
     cudaStream_t serve_stream = nullptr;
     uint32_t serve_steps = 0, serve_k = 0;
     bool serving = false;
@@ -1432,12 +1566,21 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
                                  const uint32_t* gate, const uint32_t* notify,
                                  dsq_cuda_stack** out) {
     if (!gate || !notify) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: null gate / notify");
-    uint32_t steps = 0;
+    uint32_t steps = 0, x_cols = 0;
     for (uint32_t i = 0; i < n; ++i) {
         if (gate[i] && (!deps || deps[i] >= 0))
             return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gate on chained layer %u", i);
-        if (gate[i] && i && gate[i] < gate[i - 1])
-            return fail(DSQ_E_INVALID_ARGUMENT, "served stack: gates must not decrease");
+        // every gated layer of step k sits after notify k-1 and before notify
+        // k (so gates never decrease, whatever ungated layers lie between)
+        if (gate[i] && gate[i] != steps + 1)
+            return fail(DSQ_E_INVALID_ARGUMENT,
+                        "served stack: layer %u gated on step %u lies after notify %u", i, gate[i],
+                        steps);
+        if (gate[i] && layers && layers[i]) {
+            if (x_cols && layers[i]->cols != x_cols)
+                return fail(DSQ_E_SHAPE_MISMATCH, "served stack: gated layers' cols differ");
+            x_cols = layers[i]->cols;
+        }
         if (notify[i]) {
             if (notify[i] != steps + 1)
                 return fail(DSQ_E_INVALID_ARGUMENT, "served stack: notify values must run 1, 2, ..");
@@ -1492,6 +1635,7 @@ int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, cons
         cudaSuccess)
         return bail(e, "served stack host mapping");
     S->serve_steps = steps;
+    S->serve_x_cols = x_cols;
     S->serve_y_cap = y_cap == SIZE_MAX ? 0 : y_cap;
     S->serve_x_ptr = gx;
     S->sp.serve_gate = S->serve_dev;
@@ -1511,6 +1655,11 @@ int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* y
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: x_dev / x_bytes must be 16-byte aligned, > 0");
     if (S->serve_x_ptr && x_dev != S->serve_x_ptr)
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: x_dev is not the gated layers' x buffer");
+    // CTA 0 writes exactly x_bytes into the gated layers' x every step
+    if (S->serve_x_cols &&
+        (x_bytes < size_t(S->serve_x_cols) * 2 || x_bytes > (size_t(S->serve_x_cols) * 2 + 15) / 16 * 16))
+        return fail(DSQ_E_SHAPE_MISMATCH, "serve: x_bytes %zu does not match the gated layers' %u "
+                    "fp16 columns", x_bytes, S->serve_x_cols);
     if (y_bytes % 16 || (y_bytes && (!y_host || (reinterpret_cast<uintptr_t>(y_host) & 15u))))
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: y_host / y_bytes must be 16-byte aligned");
     cudaSetDevice(S->device);
@@ -1580,8 +1729,7 @@ int dsq_cuda_serve_end(dsq_cuda_stack* S) {
     CUDA_TRY(cudaStreamSynchronize(S->serve_stream));
     uint32_t err = 0;
     CUDA_TRY(cudaMemcpy(&err, S->serve_dev + 2 * S->n + 1, 4, cudaMemcpyDeviceToHost));
-    return err ? fail(DSQ_E_INTERNAL, "serve: a step's input never arrived (wait timed out)")
-               : DSQ_OK;
+    return err ? fail(DSQ_E_INTERNAL, "serve: kernel reported an error") : DSQ_OK;
 }
 
 int dsq_cuda_stack_destroy(dsq_cuda_stack* S) {

@@ -470,6 +470,55 @@ cudaError_t launch_dense(const uint16_t* w, uint32_t rows, uint32_t cols, const 
                               static_cast<float*>(y));
 }
 
+// dequantize_layer (pipeline.cpp:49-75), second half: after the LUT dequant
+// (K6, fp32) every extracted position becomes lut_row[0] + delta, one fp32
+// addition like the reference's float arithmetic (the widened fp16 operands
+// are exact).  One warp per row, entries in CSR order.
+__global__ void apply_deltas(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
+                             const uint16_t* __restrict__ lut, uint32_t K, uint32_t rows,
+                             uint32_t cols, float* __restrict__ w) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= rows) return;
+    const float l0 = __half2float(__ushort_as_half(lut[size_t(r) * K]));
+    for (uint32_t q = row_ptr[r] + lane; q < row_ptr[r + 1]; q += 32) {
+        const uint32_t e = csr[q];
+        const float d = __half2float(__ushort_as_half(uint16_t(e >> 16)));
+        w[size_t(r) * cols + (e & 0xffffu)] = __fadd_rn(l0, d);
+    }
+}
+
+cudaError_t launch_apply_deltas(const uint32_t* row_ptr, const uint32_t* csr, const uint16_t* lut,
+                                uint32_t K, uint32_t rows, uint32_t cols, float* w,
+                                cudaStream_t st) {
+    apply_deltas<<<(rows + 7) / 8, 256, 0, st>>>(row_ptr, csr, lut, K, rows, cols, w);
+    return cudaGetLastError();
+}
+
+// dense_matvec with fp32 weights (kernels.cpp:43-47, 87-106): the products
+// double(m) * double(x) are exact, accumulated in fp64.  One warp per row.
+__global__ void dense_gemv_f32(const float* __restrict__ w, uint32_t rows, uint32_t cols,
+                               const float* __restrict__ x, double* __restrict__ y) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = gw; r < rows; r += nw) {
+        const float* wr = w + size_t(r) * cols;
+        double a = 0.0;
+        for (uint32_t c = lane; c < cols; c += 32) a = fma(double(wr[c]), double(x[c]), a);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        if (lane == 0) y[r] = a;
+    }
+}
+
+cudaError_t launch_dense_f32(const float* w, uint32_t rows, uint32_t cols, const float* x,
+                             double* y, int num_sms, cudaStream_t st) {
+    const uint32_t blocks = std::min<uint32_t>((rows + 7) / 8, uint32_t(num_sms) * 8);
+    dense_gemv_f32<<<blocks, 256, 0, st>>>(w, rows, cols, x, y);
+    return cudaGetLastError();
+}
+
 template <int BITS>
 static cudaError_t launch_decode_bits(int mode, const LayerParams& P, void* out, cudaStream_t st) {
     const size_t n = size_t(P.n_rb) * P.ng * 32;

@@ -105,6 +105,7 @@ __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int li
     }
 }
 #define mbar_wait(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
+#define mbar_wait_cons(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
 #define DSQ_WD_POLL(cond, ...)                                \
     do {                                                      \
         const unsigned long long wd0_ = gtimer_ns();          \
@@ -117,6 +118,13 @@ __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int li
         }                                                     \
     } while (0)
 #else
+// decode warps: spin on try_wait (stack.cu consumers, DSQ_CONS_SUSPEND=1 at
+// build time restores the suspend-hint wait for comparison)
+#ifdef DSQ_CONS_SUSPEND
+#define mbar_wait_cons(bar, parity) mbar_wait(bar, parity)
+#else
+#define mbar_wait_cons(bar, parity) mbar_wait_spin(bar, parity)
+#endif
 #define DSQ_WD_POLL(cond, ...)          \
     do {                                \
         while (cond) __nanosleep(20);   \
@@ -352,15 +360,13 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 // CTA 0 feeds step `gate`'s x (host doorbell -> PCIe copy ->
                 // device flag); everyone else waits for the flag
                 const uint32_t* wait_on = cta == 0 ? p.doorbell : p.serve_flag;
+                // no timeout: an idle server may wait any time for its next
+                // step, and computing on a stale x is never right -- only the
+                // host's doorbell (serve_step) or serve_end's release
+                // (0xffffffff: the steps not fed, results discarded) ends it
                 if (lane == 0 && !(cta == 0 && fed >= gate)) {
-                    const unsigned long long t0 = gtimer_ns();
-                    while ((cta == 0 ? ld_acquire_sys(wait_on) : ld_acquire_gpu(wait_on)) < gate) {
-                        if (gtimer_ns() - t0 > 10000000000ull) {
-                            atomicExch(p.serve_err, 1u);
-                            break;
-                        }
+                    while ((cta == 0 ? ld_acquire_sys(wait_on) : ld_acquire_gpu(wait_on)) < gate)
                         if (cta != 0) __nanosleep(32);  // CTA 0's polls cross PCIe anyway
-                    }
                 }
                 __syncwarp();
                 if (cta == 0 && fed < gate) {
@@ -630,6 +636,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     // read batch vector 1)
     const uint32_t xoff = tile_x_offset(lane) + (NB >= 2 ? (lane >> 4) * p.xvec : 0u);
     const uint32_t trow = (lane >> 2) & 3u;         // tile row of this lane
+    const ShiftK K{p.k29, p.k30, p.k31, p.kneg};
     const uint64_t policy = policy_evict_first();
     // this warp's weight stream: its unit range of every layer, in chunks of
     // cu units, through WS private ring slots.  The prefetch cursor (pl, pc)
@@ -701,8 +708,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         const uint32_t NS = d.ns, cu = d.cu;
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrConsStart);
         DSQ_LAP(c_top);
-        mbar_wait(&xfull[b], (l >> 1) & 1u);
-        if (l >= 2) mbar_wait(&pempty[b], ((l >> 1) - 1) & 1u);
+        mbar_wait_cons(&xfull[b], (l >> 1) & 1u);
+        if (l >= 2) mbar_wait_cons(&pempty[b], ((l >> 1) - 1) & 1u);
         DSQ_LAP(c_xw);
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrXReady);
         const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);
@@ -757,7 +764,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         uint32_t tile_c = u0 / NS, s_c = u0 - tile_c * NS;
         for (uint32_t cb = u0; cb < u1; cb += cu) {
             DSQ_LAP(c_dense);
-            if (!(p.dbg & 8u)) mbar_wait(&full[cw * WS + cslot], cphase);  // dbg 8: compute only
+            if (!(p.dbg & 8u)) mbar_wait_cons(&full[cw * WS + cslot], cphase);  // dbg 8: compute only
             DSQ_LAP(c_fw);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(cw * WS + cslot) * p.slot_bytes);
             uint32_t u = cb;
@@ -815,7 +822,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                             }
                             if constexpr (BITS == 3) {
                                 span3_mma_xn<NX>(sp[lane], sp[32 + lane], sp[64 + lane], P.a, xa0,
-                                                 xb0, ya, yb, d0, d1, ex);
+                                                 xb0, ya, yb, d0, d1, ex, K);
                             } else {
                                 span4_mma_xn<NX>(reinterpret_cast<const uint4*>(sp)[lane], P, xa0,
                                                  xb0, ya, yb, d0, d1, ex);
@@ -834,8 +841,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                             const uint4 xb0 = *reinterpret_cast<const uint4*>(xs + 128);
                             const uint4 xa1 = *reinterpret_cast<const uint4*>(xs + kSpanCols);
                             const uint4 xb1 = *reinterpret_cast<const uint4*>(xs + kSpanCols + 128);
-                            span3_mma_one(a0, a1, a2, P.a, xa0, xb0, d0);
-                            span3_mma_one(b0, b1, b2, P.a, xa1, xb1, d1);
+                            span3_mma_one(a0, a1, a2, P.a, xa0, xb0, d0, K);
+                            span3_mma_one(b0, b1, b2, P.a, xa1, xb1, d1, K);
                             sp += 2 * UW;
                             xs += 2 * kSpanCols;
                         }
@@ -850,7 +857,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         xs += kSpanCols;
                         if (k + 1 < s_end) load(sp, xs);
                         if constexpr (BITS == 3) {
-                            span3_mma(wc[0], wc[1], wc[2], P.a, xac, xbc, d0, d1);
+                            span3_mma(wc[0], wc[1], wc[2], P.a, xac, xbc, d0, d1, K);
                         } else {
                             span4_mma(make_uint4(wc[0], wc[1], wc[2], wc[3]), P, xac, xbc, d0, d1);
                         }
@@ -990,6 +997,56 @@ __global__ void decode_tiles(const uint32_t* __restrict__ idx, const uint32_t* _
         else if (MODE == 1) static_cast<uint16_t*>(out)[o] = lut[ix];
         else static_cast<float*>(out)[o] = __half2float(__ushort_as_half(lut[ix]));
     }
+}
+
+// Fragment dump (parity tests): the fp16 A fragments exactly as the product
+// kernels build them -- the same span3_frags / span4_frags decode (PRMT byte
+// planes, selector preparation) the timed stack kernel runs -- scattered back
+// to (row, col) of a dense rows x cols fp16 matrix.  One warp per unit.
+template <int BITS>
+__global__ void dump_frags(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ lutp,
+                           uint32_t rows, uint32_t cols, uint32_t tiles, uint32_t ns,
+                           uint16_t* __restrict__ out, ShiftK K) {
+    constexpr uint32_t LW = BITS == 3 ? 4u : 8u, UW = BITS * 32u;
+    const size_t unit = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (unit >= size_t(tiles) * ns) return;
+    const uint32_t tile = uint32_t(unit / ns), s = uint32_t(unit % ns);
+    const uint32_t h = lane >> 4, i = (lane >> 2) & 3u, t = lane & 3u;
+    const uint32_t* lp = lutp + (size_t(tile) * kTileRows + i) * LW;
+    Planes16 P;
+    P.a = Planes8{lp[0], lp[1], lp[2], lp[3]};
+    if constexpr (BITS == 4) P.b = Planes8{lp[4], lp[5], lp[6], lp[7]};
+    const uint32_t* sp = idx + unit * UW;
+    const uint32_t row = tile * kTileRows + i;
+    auto sink = [&](int j, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+        const uint32_t a[4] = {a0, a1, a2, a3};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const uint32_t c = s * kSpanCols + tile_col(h, t, frag_pos(j, r, hh));
+                if (row < rows && c < cols)
+                    out[size_t(row) * cols + c] = uint16_t(a[r] >> (16 * hh));
+            }
+    };
+    if constexpr (BITS == 3)
+        span3_frags(sp[lane], sp[32 + lane], sp[64 + lane], P.a, sink, K);
+    else
+        span4_frags(reinterpret_cast<const uint4*>(sp)[lane], P, sink);
+}
+
+cudaError_t launch_dump_frags(uint32_t bits, const uint32_t* idx, const uint32_t* lut,
+                              uint32_t rows, uint32_t cols, uint32_t tiles, uint32_t ns,
+                              uint16_t* out, cudaStream_t st) {
+    const ShiftK K = SQZ_SHIFTK_INIT;
+    const size_t threads = size_t(tiles) * ns * 32;
+    const uint32_t blocks = uint32_t((threads + 255) / 256);
+    if (bits == 3)
+        dump_frags<3><<<blocks, 256, 0, st>>>(idx, lut, rows, cols, tiles, ns, out, K);
+    else
+        dump_frags<4><<<blocks, 256, 0, st>>>(idx, lut, rows, cols, tiles, ns, out, K);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_decode_tiles(int mode, uint32_t bits, const uint32_t* idx, const uint32_t* lut,

@@ -98,6 +98,9 @@ struct StackParams {
     uint32_t off_part, part_rows;    // two [consumers][part_rows] dense-partial buffers
     uint32_t off_seg, seg_cap;       // two CSR scan-result buffers (floats, position-indexed)
     uint32_t smem_bytes;
+    // decode constants (tile.cuh ShiftK: 2^29, 2^30, 2^31, 0xffffffff), kept
+    // opaque to the compiler so the spare-index gather stays on the FMA pipe
+    uint32_t k29, k30, k31, kneg;
     // batch 2 (single-layer gemv): the two activation vectors share every
     // decoded A fragment -- vector b feeds the HMMA B columns 4b..4b+3, which
     // the block-diagonal map leaves free at batch 1.  x buffers, partial
@@ -131,8 +134,9 @@ struct StackParams {
     // of y system-wide before its completion release, and CTA 0 waits for the
     // layer's count, copies the layer's y (device memory) into serve_y_dst
     // over PCIe and stores k into *host_done (pinned host memory).  No CUDA
-    // call per step on the host.  A wait longer than 10 s sets *serve_err and
-    // lets the kernel run on (no hang).
+    // call per step on the host.  The gate waits have no timeout (an idle
+    // server may wait any time; a stale x is never computed on): only the
+    // host's doorbell or serve_end's release (0xffffffff) ends them.
     const uint32_t* serve_gate;
     const uint32_t* serve_notify;
     const uint32_t* doorbell;     // device-mapped pinned host word

@@ -71,64 +71,107 @@ __device__ __forceinline__ void quad16(uint32_t s, uint32_t pk, const Planes16& 
     p23 = prmt(lo, hi, 0x7362);
 }
 
-// Right shifts on the FMA pipe: k = 2^(32-s) in a register the compiler cannot
-// see through (a kernel argument), so mul.hi stays an IMAD.HI and is not
-// strength-reduced back to an ALU shift.
+// Shift / subtract constants in registers the compiler cannot see through
+// (kernel parameters set by the host, see kShiftK), so mul.hi / mad.lo stay
+// IMAD.HI / IMAD on the FMA pipe instead of being strength-reduced back to
+// ALU shifts and ANDs: k29/k30/k31 = 2^29/2^30/2^31 (mul.hi by 2^(32-s) is a
+// right shift by s), kneg = 0xffffffff (w + m * kneg = w - m).
 struct ShiftK {
-    uint32_t k29, k30, k31;
+    uint32_t k29, k30, k31, kneg;
 };
+#define SQZ_SHIFTK_INIT {1u << 29, 1u << 30, 1u << 31, 0xffffffffu}
 
-// one lane's share of one (tile, span), 3-bit: words w0..w2 -> 4 HMMAs into
-// two accumulator sets (breaks the HMMA dependency chain).  With ShiftK the
-// spare-index gather runs its three shifts as IMAD.HI (FMA pipe).
-template <bool kImadGather = false>
-__device__ __forceinline__ void span3_mma(uint32_t w0, uint32_t w1, uint32_t w2, const Planes8& P,
-                                          const uint4& xa, const uint4& xb, float (&d0)[4],
-                                          float (&d1)[4], ShiftK K = ShiftK{0, 0, 0}) {
+// The decode of one lane's share of one (tile, span) unit, written once:
+// every product variant (and the fragment dump of the parity tests,
+// stack.cu dump_frags) runs these and hands the A fragments of HMMA j
+// (j = 0..3) to its sink.
+//
+// 3-bit, words w0..w2 ("nibble + spare", layout.hpp).  ALU pipe: the three
+// selector masks m_k = w_k & 0x77777777 and the 32 PRMTs (1.09 ALU
+// instructions per weight).  FMA pipe: the spare-index gather
+//   e_k = w_k - m_k            (the bit-3 positions, IMAD with kneg)
+//   t   = e0>>3 | e1>>2 | e2>>1 (disjoint bits: three chained IMAD.HI)
+// and the hi16 selector halves (HMUL2).
+template <typename Sink>
+__device__ __forceinline__ void span3_frags(uint32_t w0, uint32_t w1, uint32_t w2,
+                                            const Planes8& P, Sink&& sink, const ShiftK& K) {
     const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
-    uint32_t t;
-    if constexpr (kImadGather) {
-        const uint32_t e0 = w0 & 0x88888888u, e1 = w1 & 0x88888888u, e2 = w2 & 0x88888888u;
-        uint32_t a, b;
-        asm("mul.hi.u32 %0, %1, %2;" : "=r"(a) : "r"(e2), "r"(K.k31));
-        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(e1), "r"(K.k30), "r"(a));
-        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(e0), "r"(K.k29), "r"(b));
-    } else {
-        t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) | ((w2 >> 1) & 0x44444444u);
-    }
+#ifdef DSQ_ALU_GATHER  // dev comparison: the gather on the ALU pipe (3 SHF + 3 LOP3)
+    (void)K;
+    const uint32_t t =
+        ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) | ((w2 >> 1) & 0x44444444u);
+#else
+    uint32_t e0, e1, e2, a, b, t;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e0) : "r"(m0), "r"(K.kneg), "r"(w0));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e1) : "r"(m1), "r"(K.kneg), "r"(w1));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e2) : "r"(m2), "r"(K.kneg), "r"(w2));
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(a) : "r"(e2), "r"(K.k31));
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(e1), "r"(K.k30), "r"(a));
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(e0), "r"(K.k29), "r"(b));
+#endif
     const uint32_t sA[4] = {m0, hi16(m0), m1, hi16(m1)};
     const uint32_t sB[4] = {m2, hi16(m2), t, hi16(t)};
-    const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         uint32_t a0, a1, a2, a3;
         quad8(sA[j], P, a0, a2);
         quad8(sB[j], P, a1, a3);
-        if (j & 1)
-            hmma16816(d1, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-        else
-            hmma16816(d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+        sink(j, a0, a1, a2, a3);
     }
+}
+
+// 4-bit: words w[0..3] (nibble n of w[k] = index 8k+n)
+template <typename Sink>
+__device__ __forceinline__ void span4_frags(const uint4& w, const Planes16& P, Sink&& sink) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t sl[4], pk[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        sl[q] = ws[q] & 0x77777777u;
+        pk[q] = ((ws[q] >> 1) & 0x44444444u) | 0x32103210u;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int wa = j >> 1, wb = 2 + (j >> 1);
+        const uint32_t sa = (j & 1) ? hi16(sl[wa]) : sl[wa];
+        const uint32_t pa = (j & 1) ? hi16(pk[wa]) : pk[wa];
+        const uint32_t sb = (j & 1) ? hi16(sl[wb]) : sl[wb];
+        const uint32_t pb = (j & 1) ? hi16(pk[wb]) : pk[wb];
+        uint32_t a0, a1, a2, a3;
+        quad16(sa, pa, P, a0, a2);
+        quad16(sb, pb, P, a1, a3);
+        sink(j, a0, a1, a2, a3);
+    }
+}
+
+// 3-bit unit -> 4 HMMAs into two accumulator sets (breaks the HMMA chain)
+__device__ __forceinline__ void span3_mma(uint32_t w0, uint32_t w1, uint32_t w2, const Planes8& P,
+                                          const uint4& xa, const uint4& xb, float (&d0)[4],
+                                          float (&d1)[4], const ShiftK& K) {
+    const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+    span3_frags(
+        w0, w1, w2, P,
+        [&](int j, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+            if (j & 1)
+                hmma16816(d1, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+            else
+                hmma16816(d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+        },
+        K);
 }
 
 // the same for one unit into a single accumulator set; two independent units
 // interleaved (span pairs) give the scheduler twice the independent work
 __device__ __forceinline__ void span3_mma_one(uint32_t w0, uint32_t w1, uint32_t w2,
                                               const Planes8& P, const uint4& xa, const uint4& xb,
-                                              float (&d)[4]) {
-    const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
-    const uint32_t t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) |
-                       ((w2 >> 1) & 0x44444444u);
-    const uint32_t sA[4] = {m0, hi16(m0), m1, hi16(m1)};
-    const uint32_t sB[4] = {m2, hi16(m2), t, hi16(t)};
+                                              float (&d)[4], const ShiftK& K) {
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        uint32_t a0, a1, a2, a3;
-        quad8(sA[j], P, a0, a2);
-        quad8(sB[j], P, a1, a3);
-        hmma16816(d, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-    }
+    span3_frags(
+        w0, w1, w2, P,
+        [&](int j, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+            hmma16816(d, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
+        },
+        K);
 }
 
 // batch 3..8: the same A fragments against NX more x sets (vector pairs
@@ -138,54 +181,31 @@ __device__ __forceinline__ void span3_mma_xn(uint32_t w0, uint32_t w1, uint32_t 
                                              const Planes8& P, const uint4& xa, const uint4& xb,
                                              const uint4 (&ya)[NX], const uint4 (&yb)[NX],
                                              float (&d0)[4], float (&d1)[4],
-                                             float (&e)[NX][2][4]) {
-    const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
-    const uint32_t t = ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) |
-                       ((w2 >> 1) & 0x44444444u);
-    const uint32_t sA[4] = {m0, hi16(m0), m1, hi16(m1)};
-    const uint32_t sB[4] = {m2, hi16(m2), t, hi16(t)};
+                                             float (&e)[NX][2][4], const ShiftK& K) {
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+    span3_frags(
+        w0, w1, w2, P,
+        [&](int j, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+            hmma16816((j & 1) ? d1 : d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        uint32_t a0, a1, a2, a3;
-        quad8(sA[j], P, a0, a2);
-        quad8(sB[j], P, a1, a3);
-        hmma16816((j & 1) ? d1 : d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-#pragma unroll
-        for (int q = 0; q < NX; ++q) {
-            const uint4& A = (j < 2) ? ya[q] : yb[q];
-            const uint32_t y0 = (j & 1) ? A.z : A.x, y1 = (j & 1) ? A.w : A.y;
-            hmma16816(e[q][j & 1], a0, a1, a2, a3, y0, y1);
-        }
-    }
+            for (int q = 0; q < NX; ++q) {
+                const uint4& A = (j < 2) ? ya[q] : yb[q];
+                const uint32_t y0 = (j & 1) ? A.z : A.x, y1 = (j & 1) ? A.w : A.y;
+                hmma16816(e[q][j & 1], a0, a1, a2, a3, y0, y1);
+            }
+        },
+        K);
 }
 
-// 4-bit: words w[0..3] (nibble n of w[k] = index 8k+n)
 __device__ __forceinline__ void span4_mma(const uint4& w, const Planes16& P, const uint4& xa,
                                           const uint4& xb, float (&d0)[4], float (&d1)[4]) {
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-    uint32_t sl[4], pk[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        sl[q] = ws[q] & 0x77777777u;
-        pk[q] = ((ws[q] >> 1) & 0x44444444u) | 0x32103210u;
-    }
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int wa = j >> 1, wb = 2 + (j >> 1);
-        const uint32_t sa = (j & 1) ? hi16(sl[wa]) : sl[wa];
-        const uint32_t pa = (j & 1) ? hi16(pk[wa]) : pk[wa];
-        const uint32_t sb = (j & 1) ? hi16(sl[wb]) : sl[wb];
-        const uint32_t pb = (j & 1) ? hi16(pk[wb]) : pk[wb];
-        uint32_t a0, a1, a2, a3;
-        quad16(sa, pa, P, a0, a2);
-        quad16(sb, pb, P, a1, a3);
+    span4_frags(w, P, [&](int j, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
         if (j & 1)
             hmma16816(d1, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
         else
             hmma16816(d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
-    }
+    });
 }
 
 template <int NX>
@@ -193,24 +213,8 @@ __device__ __forceinline__ void span4_mma_xn(const uint4& w, const Planes16& P, 
                                              const uint4& xb, const uint4 (&ya)[NX],
                                              const uint4 (&yb)[NX], float (&d0)[4],
                                              float (&d1)[4], float (&e)[NX][2][4]) {
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-    uint32_t sl[4], pk[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        sl[q] = ws[q] & 0x77777777u;
-        pk[q] = ((ws[q] >> 1) & 0x44444444u) | 0x32103210u;
-    }
     const uint32_t xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int wa = j >> 1, wb = 2 + (j >> 1);
-        const uint32_t sa = (j & 1) ? hi16(sl[wa]) : sl[wa];
-        const uint32_t pa = (j & 1) ? hi16(pk[wa]) : pk[wa];
-        const uint32_t sb = (j & 1) ? hi16(sl[wb]) : sl[wb];
-        const uint32_t pb = (j & 1) ? hi16(pk[wb]) : pk[wb];
-        uint32_t a0, a1, a2, a3;
-        quad16(sa, pa, P, a0, a2);
-        quad16(sb, pb, P, a1, a3);
+    span4_frags(w, P, [&](int j, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
         hmma16816((j & 1) ? d1 : d0, a0, a1, a2, a3, xs[2 * j], xs[2 * j + 1]);
 #pragma unroll
         for (int q = 0; q < NX; ++q) {
@@ -218,7 +222,14 @@ __device__ __forceinline__ void span4_mma_xn(const uint4& w, const Planes16& P, 
             const uint32_t y0 = (j & 1) ? A.z : A.x, y1 = (j & 1) ? A.w : A.y;
             hmma16816(e[q][j & 1], a0, a1, a2, a3, y0, y1);
         }
-    }
+    });
+}
+
+// position q (0..31) of the lane's 32 indices held by A register r (a0..a3)
+// half h of HMMA j (the block-diagonal map above): a0/a2 = piece pA,
+// a1/a3 = piece pB, a2/a3 = positions 4j+2, 4j+3
+__host__ __device__ inline uint32_t frag_pos(int j, int r, int h) {
+    return (r & 1 ? 16u : 0u) + 4u * j + (r & 2 ? 2u : 0u) + uint32_t(h);
 }
 
 // D fragments -> the 4 row sums of the tile in lanes 0, 4, 8, 12 (fixed order)

@@ -155,6 +155,10 @@ class DeviceLayer:
     def dequant(self, out_ptr: int, out_dtype: int, stream: int = 0) -> None:
         check(lib.dsq_cuda_dequant(self.handle, out_ptr, out_dtype, stream))
 
+    def dump_frags(self, out_ptr: int, stream: int = 0) -> None:
+        """fp16 A fragments of the hot decode, scattered to rows x cols (parity)."""
+        check(lib.dsq_cuda_dump_frags(self.handle, out_ptr, stream))
+
     # -- host-vector product (the reference's signature)
     def matvec_host(self, kernel: int, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float32)
@@ -385,6 +389,26 @@ def fused_dns_matvec(layer: QuantizedLayer, x, exec: Exec = Exec.cuda) -> np.nda
     """kernels.hpp:31 -- LUT product plus the CSR deltas, one device launch."""
     x = _check_x(x, layer.cols, "fused_dns_matvec")
     return device_layer(layer).matvec_host(N.KERNEL_FUSED, x)
+
+
+def dense_matvec(m, rows: int, cols: int, x, exec: Exec = Exec.cuda) -> np.ndarray:
+    """kernels.hpp:35 -- plain dense product of an fp32 matrix (fp64
+    accumulation of the exact fp32 products, dsq_cuda_dense_matvec_host)."""
+    m = np.ascontiguousarray(m, dtype=np.float32).reshape(-1)
+    if m.size != rows * cols:
+        raise DsqError(9, "dense_matvec: dimension mismatch")
+    x = np.ascontiguousarray(_check_x(x, cols, "dense_matvec"))
+    y = np.empty(rows, dtype=np.float64)
+    check(lib.dsq_cuda_dense_matvec_host(_ptr(m), rows, cols, _ptr(x), _ptr(y), 0))
+    return y
+
+
+def dequantize_layer(layer: QuantizedLayer) -> np.ndarray:
+    """pipeline.cpp:49-75 -- the represented fp32 matrix [rows, cols]: LUT
+    values, and lut_row[0] + delta (one fp32 addition) at every CSR position."""
+    w = np.empty(layer.rows * layer.cols, dtype=np.float32)
+    check(lib.dsq_cuda_dequantize_layer_host(device_layer(layer).handle, _ptr(w)))
+    return w.reshape(layer.rows, layer.cols)
 
 
 def bytes_touched_estimate(layer: QuantizedLayer) -> int:

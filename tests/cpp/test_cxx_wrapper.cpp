@@ -85,6 +85,46 @@ int main() {
         if (sqz::bytes_touched_estimate(rows, cols, 3, 0, layer.sparse.nnz()) !=
             bytes_touched_estimate(layer))
             return fail("bytes_touched_estimate", 0);
+        // the reference's free functions, namespace switched (kernels.hpp:20-79)
+        const double f_lut = normwise(sqz::lut_matvec(layer.packed, x), lut_matvec(layer.packed, x));
+        const double f_csr =
+            normwise(sqz::csr_matvec(layer.sparse, x, Exec::serial), csr_matvec(layer.sparse, x));
+        const double f_fused = normwise(sqz::fused_dns_matvec(layer, x, Exec::parallel),
+                                        fused_dns_matvec(layer, x));
+        const std::vector<float> dq = ref::dequant_dense(layer.packed);
+        const double f_dense =
+            normwise(sqz::dense_matvec(dq, rows, cols, x), dense_matvec(dq, rows, cols, x));
+        std::printf("free functions: lut %.3e csr %.3e fused %.3e dense %.3e\n", f_lut, f_csr,
+                    f_fused, f_dense);
+        if (f_lut > 1e-5) return fail("sqz::lut_matvec", f_lut);
+        if (f_csr > 1e-5) return fail("sqz::csr_matvec", f_csr);
+        if (f_fused > 1e-5) return fail("sqz::fused_dns_matvec", f_fused);
+        if (f_dense > 1e-12) return fail("sqz::dense_matvec", f_dense);
+        if (sqz::bytes_touched_estimate(layer) != bytes_touched_estimate(layer))
+            return fail("sqz::bytes_touched_estimate(layer)", 0);
+        for (BenchKernel k : {BenchKernel::lut, BenchKernel::csr, BenchKernel::fused,
+                              BenchKernel::reference}) {
+            const BenchRecord r = bench_matvec(layer, x, 3, k, Exec::parallel);
+            const sqz::BenchRecord g = sqz::bench_matvec(layer, x, 3, k, Exec::parallel);
+            if (g.kernel != r.kernel || g.repeats != 3 || g.all_seconds.size() != 3 ||
+                g.bytes_touched != r.bytes_touched || !(g.median_seconds > 0))
+                return fail("sqz::bench_matvec", double(int(k)));
+            std::printf("bench_matvec %-9s median %.1f us (reference %.1f us), %llu bytes\n",
+                        g.kernel.c_str(), g.median_seconds * 1e6, r.median_seconds * 1e6,
+                        (unsigned long long)g.bytes_touched);
+        }
+        try {
+            sqz::bench_matvec(layer, x, 2, BenchKernel::fused);
+            return fail("bench repeats < 3 accepted", 0);
+        } catch (const sqz::Error& e) {
+            if (e.errc() != int(errc::invalid_argument)) return fail("bench errc", e.errc());
+        }
+        // dequantize_layer (pipeline.cpp:49-75): bit-identical for fp16-exact layers
+        const WeightMatrix wr = dequantize_layer(layer);
+        const WeightMatrix wg = sqz::dequantize_layer<WeightMatrix>(layer);
+        if (wg.name != wr.name || wg.rows != wr.rows || wg.cols != wr.cols ||
+            wg.values != wr.values)
+            return fail("sqz::dequantize_layer", 0);
         // error mapping: a dimension mismatch is dsq::errc::shape_mismatch
         try {
             dev.fused(std::vector<float>(cols + 1));

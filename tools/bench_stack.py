@@ -36,7 +36,6 @@ MODELS = {  # hidden, intermediate, decoder layers
     "13b": (5120, 13824, 40),
     "65b": (8192, 22016, 80),
 }
-CHAIN_IN = [-1, -1, -1, 0, 3, 3, 4]  # v,q,k,o,up,gate,down (bench.py)
 
 
 def shapes(h, f):
