@@ -163,6 +163,24 @@ def cpu_reference_sample(host_layers, frac: float, repeats: int = 3):
     return total_b / total_s / 1e9, total_s, total_b, cores, desc
 
 
+def cpu_model() -> str:
+    """The host CPU model (lscpu 'Model name', else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.strip().startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def build_host_layers(seed: int = 1234):
     from oracle.oracle import make_layer
     cache = {}
@@ -198,6 +216,7 @@ def run_reference_arm(args, rank: int, world: int):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(1, "cpu"),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores,
+                         "cpu_model": cpu_model(),
                          "kind": "reference", "sample": desc},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -495,11 +514,83 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "schedule": {"workers": info.workers, "ctas": info.ctas},
         "setup_s": round(setup_s, 1),
     }
+    if world == 1 and not args.no_per_layer:
+        line["per_layer"] = per_layer_bench(dev, peak)
     if world == 1 and not args.no_cpu_baseline:
         v, s, b, cores, desc = cpu_reference_sample(host_layers, args.ref_frac, repeats=3)
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": cores,
+                                "cpu_model": cpu_model(),
                                 "kind": "reference", "sample": desc}
     print(json.dumps(line), flush=True)
+
+
+PER_LAYER = [  # (name, rows, cols, bits, sparsity): BASELINE configs[0] and configs[1]
+    ("configs0_4096x4096_4bit_dense", 4096, 4096, 4, 0.0),
+    ("configs1_4096x4096_3bit_s045", 4096, 4096, 3, SPARSITY),
+    ("configs1_11008x4096_3bit_s045", 11008, 4096, 3, SPARSITY),
+    ("configs1_4096x11008_3bit_s045", 4096, 11008, 3, SPARSITY),
+]
+
+
+def per_layer_bench(dev, peak: float, launches: int = 200) -> dict:
+    """µs per layer (the metric's first item) for single-layer products:
+    `isolated` = one dsq_cuda_gemv launch per product (K launches back to back
+    under PDL, captured in a CUDA graph so host launch cost is not timed);
+    `in_stack` = the same products as independent layers of one persistent
+    launch.  Weights rotate over copies totalling > 128 MB (> L2).  CUDA
+    events on the launching stream."""
+    import torch
+    import paper_2306_07629_b200._native as N
+    from paper_2306_07629_b200 import DeviceLayer, DeviceStack
+    from oracle.oracle import make_layer, make_x, to_quantized_layer
+    out = {}
+    st = torch.cuda.current_stream(dev)
+    for name, rows, cols, bits, sp in PER_LAYER:
+        L = make_layer(rows, cols, bits, sp, seed=rows + cols + bits)
+        q = to_quantized_layer(L, name=name)
+        nbytes = int(N.lib.dsq_bytes_touched_estimate(rows, cols, bits, 0, L.nnz))
+        ncopy = max(4, -(-(160 << 20) // nbytes))
+        dls = [DeviceLayer(q, device=dev.index or 0) for _ in range(ncopy)]
+        x = torch.from_numpy(make_x(cols).view(np.int16)).to(dev)
+        ys = [torch.empty(rows, dtype=torch.int16, device=dev) for _ in range(ncopy)]
+
+        def launch_all(k):
+            for i in range(k):
+                dls[i % ncopy].gemv(N.KERNEL_FUSED, x.data_ptr(), N.F16, ys[i % ncopy].data_ptr(),
+                                    N.F16, st.cuda_stream)
+        launch_all(ncopy)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            launch_all(launches)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        us_iso = e0.elapsed_time(e1) * 1e3 / launches
+        stk = DeviceStack(dls * max(1, launches // ncopy), [-1] * (ncopy * max(1, launches // ncopy)),
+                          [x.data_ptr()] * (ncopy * max(1, launches // ncopy)),
+                          [y.data_ptr() for y in ys] * max(1, launches // ncopy), N.F16)
+        n_in = ncopy * max(1, launches // ncopy)
+        stk.run(st.cuda_stream)
+        torch.cuda.synchronize()
+        e0.record(st)
+        stk.run(st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        us_stk = e0.elapsed_time(e1) * 1e3 / n_in
+        gbs_iso, gbs_stk = nbytes / us_iso / 1e3, nbytes / us_stk / 1e3
+        out[name] = {"algorithmic_bytes": nbytes, "copies_rotated": ncopy,
+                     "isolated_us": round(us_iso, 3), "isolated_GBs": round(gbs_iso, 1),
+                     "isolated_frac": round(gbs_iso / peak, 4),
+                     "in_stack_us": round(us_stk, 3), "in_stack_GBs": round(gbs_stk, 1),
+                     "in_stack_frac": round(gbs_stk / peak, 4)}
+        del g, stk, dls
+        torch.cuda.synchronize()
+    return out
 
 
 class TPUnavailable(RuntimeError):
@@ -697,6 +788,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-layer", action="store_true",
+                    help="skip the single-layer µs/layer section (configs[0], configs[1] shapes)")
     ap.add_argument("--ref-frac", type=float, default=1 / 16,
                     help="row fraction of each GEMV in the CPU sample")
     args = ap.parse_args()
@@ -716,13 +809,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         if use_tp:
-            try:
-                run_ours_tp(args, rank, world, local_rank)
-                return
-            except TPUnavailable as e:
-                if rank == 0:
-                    print(f"tensor parallelism unavailable ({e}); running replicas",
-                          file=sys.stderr)
+            # a TP failure is an error (exit non-zero), never a silent switch to
+            # replicas: --multi replicas asks for replicas explicitly
+            run_ours_tp(args, rank, world, local_rank)
+            return
         run_ours(args, rank, world, local_rank)
     finally:
         if world > 1 or args.force_tp:

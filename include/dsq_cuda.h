@@ -295,7 +295,8 @@ int dsq_cuda_stack_destroy(dsq_cuda_stack* stack);
 
 /* ---- tensor parallelism: the all-reduce fused into the stack -- */
 /* One context per rank (one process per GPU): a receive buffer for the
- * partial outputs of row-parallel layers ([2][world][max_rows] fp32) and
+ * partial outputs of row-parallel layers ([2][world][max_rows] 64-bit words
+ * {fp32 value, u32 tag}, single-copy atomic, so no separate flag) and
  * per-CTA arrival flags, shared with the peers through CUDA IPC
  * (ipc_handle_out: 64 bytes, cudaIpcMemHandle_t; exchange them with any
  * out-of-band channel, e.g. torch.distributed all_gather, then

@@ -295,7 +295,10 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     // each a whole number of units (384 B 3-bit, 512 B 4-bit)
     const uint32_t ub = unit_words(bits) * 4;
     const size_t ring = size_t(smax) > sp.off_ring ? size_t(smax) - sp.off_ring : 0;
-    sp.n_slots = sp.consumers * 2;
+    uint32_t ws = kWarpSlotsDefault;
+    if (const char* e = std::getenv("DSQ_STACK_SLOTS"))
+        ws = std::max<uint32_t>(2, std::min<uint32_t>(kMaxWarpSlots, uint32_t(atoi(e))));
+    sp.n_slots = sp.consumers * ws;
     sp.slot_bytes = uint32_t(ring / sp.n_slots / ub * ub);
     if (sp.slot_bytes < 2 * ub) {
         // large batched x: retry with one shared x buffer before giving up
@@ -1169,7 +1172,7 @@ int dsq_cuda_csr_matvec_host(const dsq_csr_view* s, const float* x, double* y, i
 struct dsq_cuda_tp {
     int device = 0;
     uint32_t world = 1, rank = 0, max_rows = 0, max_grid = 0;
-    void* buf = nullptr;           // recv [2][world][max_rows] fp32 + flags [max_grid] u32
+    void* buf = nullptr;           // recv [2][world][max_rows] {fp32, u32 tag} + flags [max_grid] u32
     size_t recv_bytes = 0;
     uint64_t base = 0;             // reduce ordinals completed by earlier launches
     void* peer_base[8] = {};       // mapped peer buffers (own: buf)

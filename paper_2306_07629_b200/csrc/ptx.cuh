@@ -127,6 +127,23 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+// role-warp wait off the critical path: a non-blocking probe, then a plain
+// nanosleep (not woken by unrelated mbarrier traffic, unlike the suspend
+// hint's NANOSLEEP.SYNCS) so a long wait costs a few issue slots per
+// `ns`, not a probe loop the decoding warps pay for
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    while (!mbar_test_wait(bar, parity)) __nanosleep(ns);
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -51,7 +51,7 @@ namespace sqz {
 // are done with the layer.  Descriptors of long stacks live in global memory,
 // and re-reading them per field from every warp is slow.
 constexpr uint32_t kDescSlots = 8;
-constexpr uint32_t kWarpSlots = 2;  // ring slots per consumer warp
+// ring slots per consumer warp: p.n_slots / consumers (host plan, 2..kMaxWarpSlots)
 // CSR warps: p.csr_warps (1..kCsrWarps) process the CSR deltas -- chosen per
 // plan from the largest per-CTA entry count (each extra role warp costs the
 // decoding warps issue slots, so light outlier loads get fewer)
@@ -83,6 +83,15 @@ __device__ __forceinline__ Share cta_share(const StackLayerDesc& d, uint32_t cta
     return s;
 }
 
+// dev-only experiment switches (StackParams::dbg bits 1 / 8 skip the decode
+// math / the weight loads): compiled in only with -DDSQ_STACK_DEV (the
+// variant-lib / profile builds), so the product library can never skip work
+#if defined(DSQ_STACK_DEV) || defined(DSQ_STACK_PROFILE)
+constexpr bool kDevSwitches = true;
+#else
+constexpr bool kDevSwitches = false;
+#endif
+
 __device__ __forceinline__ unsigned long long gtimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -106,6 +115,8 @@ __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int li
 }
 #define mbar_wait(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
 #define mbar_wait_cons(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
+#define mbar_wait_role(bar, parity, ns) mbar_wait_wd(bar, parity, __LINE__)
+#define mbar_wait_fin(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
 #define DSQ_WD_POLL(cond, ...)                                \
     do {                                                      \
         const unsigned long long wd0_ = gtimer_ns();          \
@@ -118,13 +129,31 @@ __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int li
         }                                                     \
     } while (0)
 #else
-// decode warps: spin on try_wait (stack.cu consumers, DSQ_CONS_SUSPEND=1 at
-// build time restores the suspend-hint wait for comparison)
-#ifdef DSQ_CONS_SUSPEND
-#define mbar_wait_cons(bar, parity) mbar_wait(bar, parity)
-#else
+// decode warps: the suspend-hint wait (DSQ_CONS_SPIN: plain try_wait spin,
+// measured neutral)
+#ifdef DSQ_CONS_SPIN
 #define mbar_wait_cons(bar, parity) mbar_wait_spin(bar, parity)
+#else
+#define mbar_wait_cons(bar, parity) mbar_wait(bar, parity)
 #endif
+// role-warp waits (publisher / loader: off the critical path; finishing and
+// CSR warps: DSQ_FIN_SLEEP ns, 0 = the suspend-hint wait)
+#ifndef DSQ_ROLE_SLEEP
+#define DSQ_ROLE_SLEEP 1
+#endif
+#ifndef DSQ_FIN_SLEEP
+#define DSQ_FIN_SLEEP 0
+#endif
+#define mbar_wait_role(bar, parity, ns)                                     \
+    do {                                                                    \
+        if (DSQ_ROLE_SLEEP) mbar_wait_sleep(bar, parity, (ns));             \
+        else mbar_wait(bar, parity);                                        \
+    } while (0)
+#define mbar_wait_fin(bar, parity)                                          \
+    do {                                                                    \
+        if (DSQ_FIN_SLEEP) mbar_wait_sleep(bar, parity, DSQ_FIN_SLEEP);      \
+        else mbar_wait(bar, parity);                                        \
+    } while (0)
 #define DSQ_WD_POLL(cond, ...)          \
     do {                                \
         while (cond) __nanosleep(20);   \
@@ -203,7 +232,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     constexpr uint32_t UW = BITS * 32u;             // words per (tile, span) unit
     extern __shared__ __align__(1024) uint8_t sm[];
     // mbarriers: per-warp ring slots, then per buffer parity b in {0,1}
-    constexpr uint32_t WS = kWarpSlots;
+    const uint32_t WS = p.n_slots / NC;
     uint64_t* full = reinterpret_cast<uint64_t*>(sm);  // [NC][WS] unit chunk landed
     uint64_t* xfull = full + NC * WS;      // x + LUT planes staged (TMA transaction count)
     uint64_t* cfull = xfull + 2;           // CSR slice staged (TMA transaction count)
@@ -252,7 +281,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         pdl_trigger();
         for (uint32_t l = 0; l < p.n_layers; ++l) {
             const uint32_t k = l % kDescSlots;
-            if (l >= kDescSlots) mbar_wait(&dempty[k], ((l / kDescSlots) - 1) & 1u);
+            if (l >= kDescSlots) mbar_wait_role(&dempty[k], ((l / kDescSlots) - 1) & 1u, 2000);
             const StackLayerDesc& gd = layer_desc(p, l);
             uint32_t* dst = reinterpret_cast<uint32_t*>(&sdesc[k]);
             constexpr uint32_t kDW = sizeof(StackLayerDesc) / 4;
@@ -278,8 +307,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         uint32_t fed = 0;  // served stacks: the last step whose x CTA 0 copied in
         for (uint32_t l = 0; l < p.n_layers; ++l) {
             const uint32_t b = l & 1u;
-            if (l >= 2) mbar_wait(&bempty[b], ((l >> 1) - 1) & 1u);
-            const SDesc& sd = desc_wait(l);
+            if (l >= 2) mbar_wait_role(&bempty[b], ((l >> 1) - 1) & 1u, 500);
+            mbar_wait_role(&dfull[l % kDescSlots], (l / kDescSlots) & 1u, 200);
+            const SDesc& sd = sdesc[l % kDescSlots];
             const StackLayerDesc& d = sd.d;
             const Share sh = cta_share(d, cta);
             const uint32_t r0 = sh.r0, r1 = sh.r0 + sh.nrows;
@@ -425,7 +455,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         const Share sh = cta_share(d, cta);
         const uint32_t r0 = sh.r0, nrows = sh.nrows;
         const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
-        mbar_wait(&pfull[b], ph);
+        mbar_wait_fin(&pfull[b], ph);
         if (f == 0 && lane == 0) DSQ_TRACE(l, kTrAllDense);
         // the CSR scan results (position-indexed, see csr_stream)
         const uint32_t ea = sd.e0 & ~3u;
@@ -593,9 +623,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             const uint32_t b = l & 1u, ph = (l >> 1) & 1u;
             const SDesc& sd = desc_wait(l);
             const Share sh = cta_share(sd.d, cta);
-            mbar_wait(&xfull[b], ph);
-            mbar_wait(&cfull[b], ph);
-            if (l >= 2) mbar_wait(&pempty[b], ((l >> 1) - 1) & 1u);  // segs consumed
+            mbar_wait_fin(&xfull[b], ph);
+            mbar_wait_fin(&cfull[b], ph);
+            if (l >= 2) mbar_wait_fin(&pempty[b], ((l >> 1) - 1) & 1u);  // segs consumed
             if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrStaged);
             const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);
             const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
@@ -663,7 +693,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
             if (pa < pe) {
                 const uint32_t n = min(pcu, pe - pa);
-                if (lane == 0 && !(p.dbg & 8u)) {
+                if (lane == 0 && !(kDevSwitches && (p.dbg & 8u))) {
                     uint64_t* bar = &full[cw * WS + pslot];
                     mbar_arrive_expect_tx(bar, n * UW * 4);
                     bulk_g2s(ring + size_t(cw * WS + pslot) * p.slot_bytes, psrc, n * UW * 4, bar,
@@ -764,12 +794,13 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         uint32_t tile_c = u0 / NS, s_c = u0 - tile_c * NS;
         for (uint32_t cb = u0; cb < u1; cb += cu) {
             DSQ_LAP(c_dense);
-            if (!(p.dbg & 8u)) mbar_wait_cons(&full[cw * WS + cslot], cphase);  // dbg 8: compute only
+            if (!(kDevSwitches && (p.dbg & 8u)))  // dev bit 8: compute only
+                mbar_wait_cons(&full[cw * WS + cslot], cphase);
             DSQ_LAP(c_fw);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(cw * WS + cslot) * p.slot_bytes);
             uint32_t u = cb;
             const uint32_t ue = min(u1, cb + cu);
-            if (!(p.dbg & 1u)) {
+            if (!(kDevSwitches && (p.dbg & 1u))) {  // dev bit 1: streaming only
                 uint32_t tile = tile_c, s = s_c;
                 const uint32_t* sp = chunk;
                 while (u < ue) {
@@ -944,6 +975,20 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl) {
                                              max_optin);
         if (e != cudaSuccess) return e;
         if (dev >= 0 && dev < 64) attr_done[bi][dev] = true;
+    }
+    // every grid-wide wait in the kernel (layer completion counters, the TP
+    // exchange, the serving flags) assumes all CTAs are co-resident: check
+    // that one CTA of this size fits per SM and that the grid does not
+    // exceed the SM count (cooperative-launch guarantee, without the
+    // cooperative attribute, which programmatic dependent launch excludes)
+    {
+        int per_sm = 0, sms = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, kern, int(cfg.blockDim.x), cfg.dynamicSmemBytes);
+        if (e != cudaSuccess) return e;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (per_sm < 1 || uint64_t(p.grid) > uint64_t(per_sm) * uint64_t(sms))
+            return cudaErrorCooperativeLaunchTooLarge;
     }
     return cudaLaunchKernelEx(&cfg, kern, p);
 }

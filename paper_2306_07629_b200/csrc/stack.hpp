@@ -42,6 +42,8 @@ constexpr uint32_t kNoDep = 0xffffffffu;
 constexpr uint32_t kInlineLayers = 8;  // layer descs carried in the launch params
 constexpr uint32_t kTileRows = 4;
 constexpr uint32_t kSpanCols = 256;
+constexpr uint32_t kWarpSlotsDefault = 2;  // TMA ring slots per consumer warp (DSQ_STACK_SLOTS)
+constexpr uint32_t kMaxWarpSlots = 6;      // mbarrier area: 16 x 6 + 30 barriers in 1 KB
 
 // span column (0..255) of index position q (0..31) of lane (h, i, t): the
 // lane covers pieces 4h+t (q < 16) and 8+4h+t (q >= 16); piece p is columns

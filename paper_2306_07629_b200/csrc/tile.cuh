@@ -87,20 +87,21 @@ struct ShiftK {
 // (j = 0..3) to its sink.
 //
 // 3-bit, words w0..w2 ("nibble + spare", layout.hpp).  ALU pipe: the three
-// selector masks m_k = w_k & 0x77777777 and the 32 PRMTs (1.09 ALU
-// instructions per weight).  FMA pipe: the spare-index gather
-//   e_k = w_k - m_k            (the bit-3 positions, IMAD with kneg)
-//   t   = e0>>3 | e1>>2 | e2>>1 (disjoint bits: three chained IMAD.HI)
-// and the hi16 selector halves (HMUL2).
+// selector masks m_k = w_k & 0x77777777, the spare-index gather
+// t = (w0>>3 & 0x1..) | (w1>>2 & 0x2..) | (w2>>1 & 0x4..) and the 32 PRMTs;
+// FMA pipe: the hi16 selector halves (HMUL2).  (DSQ_IMAD_GATHER moves the
+// gather to the FMA pipe -- e_k = w_k - m_k by IMAD, three chained IMAD.HI --
+// which cuts 6 ALU instructions per unit but measured 6% slower on B200: the
+// unit loop is bound by issue latency, not by the ALU pipe.)
 template <typename Sink>
 __device__ __forceinline__ void span3_frags(uint32_t w0, uint32_t w1, uint32_t w2,
                                             const Planes8& P, Sink&& sink, const ShiftK& K) {
     const uint32_t m0 = w0 & 0x77777777u, m1 = w1 & 0x77777777u, m2 = w2 & 0x77777777u;
-#ifdef DSQ_ALU_GATHER  // dev comparison: the gather on the ALU pipe (3 SHF + 3 LOP3)
+#ifndef DSQ_IMAD_GATHER  // the gather on the ALU pipe (3 SHF + 3 LOP3); see below
     (void)K;
     const uint32_t t =
         ((w0 >> 3) & 0x11111111u) | ((w1 >> 2) & 0x22222222u) | ((w2 >> 1) & 0x44444444u);
-#else
+#else  // dev variant: on the FMA pipe -- measured 6% slower (longer dependency chain)
     uint32_t e0, e1, e2, a, b, t;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e0) : "r"(m0), "r"(K.kneg), "r"(w0));
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e1) : "r"(m1), "r"(K.kneg), "r"(w1));
