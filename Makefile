@@ -6,7 +6,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas 
 PKG       := paper_2306_07629_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libdsq_cuda.so
-OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o
+OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 
 all: $(LIB) oracle cxx-test
 
@@ -35,6 +35,9 @@ $(CSRC)/decompose.o: $(CSRC)/decompose.cu
 $(CSRC)/quantize_api.o: $(CSRC)/quantize_api.cpp $(CSRC)/quantize.hpp include/dsq_cuda.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -c $< -o $@
 
+$(CSRC)/shard.o: $(CSRC)/shard.cpp include/dsq_cuda.h
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -c $< -o $@
+
 $(CSRC)/roofline.o: $(CSRC)/roofline.cpp include/dsq_cuda.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -c $< -o $@
 
@@ -47,7 +50,7 @@ PROFLIB := $(PKG)/libdsq_cuda_prof.so
 profile-lib: $(PROFLIB)
 $(CSRC)/stack_prof.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_PROFILE -c $< -o $@ 2> /dev/null
-$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o
+$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 # debug variant: bounded waits that trap with the waiting site (stack.cu)
@@ -55,7 +58,7 @@ WDLIB := $(PKG)/libdsq_cuda_wd.so
 watchdog-lib: $(WDLIB)
 $(CSRC)/stack_wd.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_WATCHDOG -c $< -o $@
-$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o
+$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 oracle:

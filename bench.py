@@ -597,107 +597,167 @@ class TPUnavailable(RuntimeError):
     pass
 
 
+MODELS = {"7b": (4096, 11008, 32), "65b": (8192, 22016, 80)}  # hidden, ffn, decoder layers
+
+
+def model_shapes(model: str):
+    h, f, _ = MODELS[model]
+    return [("v", h, h), ("q", h, h), ("o", h, h), ("k", h, h), ("up", f, h), ("gate", f, h),
+            ("down", h, f)]
+
+
+def synthetic_layer(rows, cols, seed, bits=BITS, sparsity=SPARSITY):
+    """A QuantizedLayer generated directly in the reference packed layout
+    (uniform 3-bit indices = uniform payload bytes; outlier positions cleared
+    to index 0 as quantize_layer does, pipeline.cpp:25-32), so 65B shapes
+    build in seconds (bench setup only)."""
+    from paper_2306_07629_b200 import CsrMatrix, PackedDense, QuantizedLayer
+    from oracle.oracle import nnz_for
+    rng = np.random.default_rng(seed)
+    stride = (cols * bits + 7) // 8
+    payload = rng.integers(0, 256, size=rows * stride, dtype=np.uint8)
+    luts = np.sort(rng.normal(0.0, 0.02, size=(rows, 1 << bits)).astype(np.float16),
+                   axis=1).reshape(-1)
+    pos = np.unique(rng.integers(0, rows * cols, size=nnz_for(rows * cols, sparsity),
+                                 dtype=np.int64))
+    r, c = pos // cols, pos % cols
+    for b in range(bits):
+        bp = r * stride * 8 + c * bits + b
+        np.bitwise_and.at(payload, bp >> 3, np.uint8(0xff) ^ (np.uint8(1) << (bp & 7).astype(np.uint8)))
+    row_ptr = np.zeros(rows + 1, np.uint32)
+    np.add.at(row_ptr, r + 1, 1)
+    row_ptr = np.cumsum(row_ptr, dtype=np.uint64).astype(np.uint32)
+    vals = rng.normal(0.0, 0.2, size=pos.size).astype(np.float16)
+    return QuantizedLayer(f"{rows}x{cols}", rows, cols, PackedDense(bits, rows, cols, luts, payload),
+                          CsrMatrix(rows, cols, row_ptr, c.astype(np.uint16), vals), 10)
+
+
 def run_ours_tp(args, rank: int, world: int, local_rank: int):
-    """N GPUs, one decoder-layer chain tensor-parallel over all of them
-    (Megatron split: v,q,k,up,gate column-parallel, o,down row-parallel),
-    the two all-reduces per decoder layer fused into the persistent stack
-    kernel over NVLink peer memory (CUDA IPC-mapped receive buffers, per-CTA
-    release/acquire flags at system scope).  value = the whole model's
-    reference-charged bytes per step / step time (strong scaling)."""
+    """A decoder-layer chain of `--workload` shapes (65B by default at N > 1:
+    BASELINE configs[3]) tensor-parallel over the N GPUs (Megatron split:
+    v,q,k,up,gate column-parallel, o,down row-parallel, tp.py), the two
+    all-reduces per decoder layer fused into the persistent stack kernel over
+    NVLink peer memory (CUDA IPC-mapped receive buffers).  Each rank generates
+    its own shards of the layer shapes directly (synthetic weights).  value =
+    the whole decoder layer's reference-charged bytes per step / step time,
+    max over ranks (strong scaling: the model is fixed, N GPUs share it)."""
     import torch
     import torch.distributed as dist
     import paper_2306_07629_b200._native as N
     from paper_2306_07629_b200 import DeviceLayer, DeviceStack
     from paper_2306_07629_b200.dsq import TPContext
-    from paper_2306_07629_b200.tp import decoder_chain, shard_decoder
-    from oracle.oracle import make_x, to_quantized_layer
+    from paper_2306_07629_b200.tp import ROW_PARALLEL, decoder_chain, split_range
+    from oracle.oracle import make_x, nnz_for
 
+    model = args.workload if args.workload != "auto" else "65b"
+    h, f, n_dec = MODELS[model]
+    shapes = model_shapes(model)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     t_setup = time.time()
-    host_layers = build_host_layers()
-    qls = [to_quantized_layer(L, name=n) for L, (n, _, _) in zip(host_layers, SHAPES)]
-    bytes_step = sum(int(N.lib.dsq_bytes_touched_estimate(r, c, BITS, 0, L.nnz))
-                     for L, (_, r, c) in zip(host_layers, SHAPES))
-    shards = shard_decoder(qls, rank, world)
-    n_rot = args.rotation
+    bytes_step = sum(int(N.lib.dsq_bytes_touched_estimate(r, c, BITS, 0,
+                                                          nnz_for(r * c, SPARSITY)))
+                     for _, r, c in shapes)
+    # this rank's shard shapes (32-aligned splits, tp.shard_decoder's)
+    shard_shapes = []
+    for name, r, c in shapes:
+        if world == 1:
+            shard_shapes.append((r, c))
+        elif name in ROW_PARALLEL:
+            c0, c1 = split_range(c, world, rank, 32)
+            shard_shapes.append((r, c1 - c0))
+        else:
+            r0, r1 = split_range(r, world, rank, 32)
+            shard_shapes.append((r1 - r0, c))
+    cache = {}
+    shards = []
+    for i, (r, c) in enumerate(shard_shapes):
+        if (r, c) not in cache:
+            cache[(r, c)] = synthetic_layer(r, c, seed=1000 * rank + r * 7 + c)
+        shards.append(cache[(r, c)])
+    shard_bytes = sum(int(N.lib.dsq_bytes_touched_estimate(q.rows, q.cols, BITS, 0,
+                                                           q.sparse.nnz())) for q in shards)
+    # rotation: distinct device weights per step totalling > 2x L2 per GPU
+    n_rot = max(2, -(-(256 << 20) // shard_bytes)) if args.rotation_auto else args.rotation
     dls = [[DeviceLayer(q, device=local_rank) for q in shards] for _ in range(n_rot)]
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    ctx = TPContext(world, rank, max_rows=max(r for _, r, _ in SHAPES), max_grid=sms,
-                    device=local_rank)
-    handles = [None] * world
-    dist.all_gather_object(handles, ctx.ipc_handle)
-    ok = 1
-    try:
-        ctx.connect(handles)
-    except Exception as e:  # P2P / IPC unavailable: every rank falls back together
-        print(f"rank {rank}: tp connect failed: {e}", file=sys.stderr)
-        ok = 0
-    flag = torch.tensor([ok], device=dev)
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    if not int(flag.item()):
-        raise TPUnavailable("CUDA IPC peer mapping failed")
+    ctx = None
+    if world > 1:
+        ctx = TPContext(world, rank, max_rows=h, max_grid=sms, device=local_rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, ctx.ipc_handle)
+        ok = 1
+        try:
+            ctx.connect(handles)
+        except Exception as e:
+            print(f"rank {rank}: tp connect failed: {e}", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            raise TPUnavailable("CUDA IPC peer mapping failed")
     st = torch.cuda.Stream(dev)
     torch.cuda.set_stream(st)
     sp = st.cuda_stream
-    x = torch.from_numpy(make_x(4096, seed=100).view(np.int16)).to(dev)
+    x = torch.from_numpy(make_x(h, seed=100).view(np.int16)).to(dev)
     ys = [[torch.empty(q.rows, dtype=torch.int16, device=dev) for q in shards]
           for _ in range(n_rot)]
 
     def build(nsteps, offset):
         deps, reduce, _ = decoder_chain(nsteps, 1)
         layers, yp = [], []
-        for s in range(nsteps):
-            slot = (offset + s) % n_rot
+        for s_ in range(nsteps):
+            slot = (offset + s_) % n_rot
             layers += dls[slot]
             yp += [y.data_ptr() for y in ys[slot]]
         xp = [x.data_ptr() if d < 0 else 0 for d in deps]
+        if ctx is None:
+            return DeviceStack(layers, deps, xp, yp, N.F16)
         return DeviceStack(layers, deps, xp, yp, N.F16, reduce=reduce, tp=ctx)
 
     s_warm, s_time = build(args.warmup, 0), build(args.steps, args.warmup)
-    # every rank runs the same launch sequence (the reduce flag targets
-    # advance per launch): fixed counts, no time-based loops
+    # every rank runs the same launch sequence (the reduce tags advance per
+    # launch): fixed counts, no time-based loops
     for _ in range(2):
         s_warm.run(sp)
     torch.cuda.synchronize()
-    # validate the fused reduce on this machine before timing it: no
-    # watchdog event, and every rank holds the same reduced outputs (the
-    # last step's o and down); otherwise all ranks fall back to replicas
-    ok = 1
-    try:
-        ctx.check()
-    except Exception as e:
-        print(f"rank {rank}: tp watchdog: {e}", file=sys.stderr)
-        ok = 0
-    slot = (args.warmup - 1) % n_rot
-    o_i = [n for n, _, _ in SHAPES].index("o")
-    sig = torch.stack([ys[slot][o_i].to(torch.int64).sum(), ys[slot][6].to(torch.int64).sum()])
-    sigs = [torch.zeros_like(sig) for _ in range(world)]
-    dist.all_gather(sigs, sig)
-    if any(not torch.equal(g, sigs[0]) for g in sigs):
-        ok = 0
-    flag = torch.tensor([ok], device=dev)
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    if not int(flag.item()):
-        raise TPUnavailable("fused TP reduce failed validation (watchdog or rank mismatch)")
+    if ctx is not None:
+        # validate the fused reduce before timing: no watchdog event and the
+        # same reduced outputs (the last step's o and down) on every rank
+        ok = 1
+        try:
+            ctx.check()
+        except Exception as e:
+            print(f"rank {rank}: tp watchdog: {e}", file=sys.stderr)
+            ok = 0
+        slot = (args.warmup - 1) % n_rot
+        sig = torch.stack([ys[slot][2].to(torch.int64).sum(), ys[slot][6].to(torch.int64).sum()])
+        sigs = [torch.zeros_like(sig) for _ in range(world)]
+        dist.all_gather(sigs, sig)
+        if any(not torch.equal(g, sigs[0]) for g in sigs):
+            ok = 0
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            raise TPUnavailable("fused TP reduce failed validation (watchdog or rank mismatch)")
     setup_s = time.time() - t_setup
     sampler = ClockSampler(local_rank)
     sampler.start()
-    # soak for ~args.soak seconds; the run count is agreed across ranks so the
-    # fused-reduce launches stay paired
     t0 = time.time()
     s_warm.run(sp)
     torch.cuda.synchronize()
     per_run = max(time.time() - t0, 1e-5)
     n_soak = torch.tensor([int(args.soak / per_run) + 1], device=dev, dtype=torch.int64)
-    dist.all_reduce(n_soak, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(n_soak, op=dist.ReduceOp.MAX)
     for i in range(int(n_soak.item())):
         s_warm.run(sp)
         if i % 64 == 63:
             torch.cuda.synchronize()
     torch.cuda.synchronize()
     s_warm.run(sp)
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -705,21 +765,25 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
     s_time.run(sp)
     e1.record(st)
     torch.cuda.synchronize()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     ms = e0.elapsed_time(e1)
     clocks = sampler.stop()
-    ctx.check()
+    if ctx is not None:
+        ctx.check()
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_step = ms / args.steps
     value = bytes_step * args.steps / (ms * 1e-3) / 1e9
 
-    # e2e: one-step TP stacks from host memory (x H2D, step output D2H)
+    # e2e: one-step stacks from host memory (x H2D, the step's reduced down
+    # output D2H) through DeviceStack.run on every rank
     e2e = None
     if not args.no_e2e:
         one = [build(1, slot) for slot in range(n_rot)]
-        x_host = torch.from_numpy(make_x(4096, seed=7).view(np.int16)).pin_memory()
+        x_host = torch.from_numpy(make_x(h, seed=7).view(np.int16)).pin_memory()
         y_host = torch.empty(shards[-1].rows, dtype=torch.int16).pin_memory()
 
         def step(slot):
@@ -728,22 +792,25 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
             y_host.copy_(ys[slot][-1], non_blocking=True)
             st.synchronize()
 
-        for s in range(3):
-            step(s % n_rot)
-        dist.barrier()
+        for s_ in range(3):
+            step(s_ % n_rot)
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        for s in range(args.e2e_steps):
-            step(s % n_rot)
+        for s_ in range(args.e2e_steps):
+            step(s_ % n_rot)
         el = time.perf_counter() - t0
         t = torch.tensor([el], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
-        ctx.check()
+        if ctx is not None:
+            ctx.check()
         e2e = {"value": round(bytes_step * args.e2e_steps / el / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": 4096 * 2, "d2h_bytes_per_step": shards[-1].rows * 2,
+               "h2d_bytes_per_step": h * 2, "d2h_bytes_per_step": shards[-1].rows * 2,
                "steps": args.e2e_steps, "ms_per_step": round(el / args.e2e_steps * 1e3, 4),
                "api": "DeviceStack.run (dsq_cuda_stack_create_tp) per decoder-layer step on "
-                      "every rank, pinned host x -> device, step output -> host"}
+                      "every rank: pinned host x -> device, the step's reduced output -> host"}
     if rank != 0:
         return
     pk = peaks()
@@ -753,17 +820,29 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16",
-        "data": "synthetic (random fp16 centroids/indices/deltas; weights random-init)",
-        "config": workload_config(n_rot, f"tp{world} (fused all-reduce over NVLink peer memory)"),
-        "us_per_layer": round(ms_step * 1e3 / len(SHAPES), 3),
-        "decode_tok_s_linear": round(1e3 / (ms_step * LLAMA7B_LAYERS), 1),
+        "data": "synthetic (random fp16 centroids/indices/deltas per rank shard; "
+                "weights random-init)",
+        "config": {
+            "workload": f"llama{model[:-1]}-decoder-linear-chain tensor-parallel: q,k,v,o "
+                        f"{h}x{h}; gate,up {f}x{h}; down {h}x{f}; 3-bit LUT + 0.45% CSR; batch 1 "
+                        f"(BASELINE configs[3] for 65b)",
+            "gemvs_per_step": 7, "bits": BITS, "sparsity": SPARSITY, "batch": 1,
+            "l2": f"inputs larger than L2: rotation over {n_rot} decoder layers of distinct "
+                  f"device weights ({shard_bytes * n_rot / 2**20:.0f} MiB per GPU)",
+            "parallelism": f"tp{world} (v,q,k,up,gate column-parallel; o,down row-parallel; "
+                           f"all-reduce fused into the stack kernel over NVLink peer memory)"
+            if world > 1 else "tp1"},
+        "us_per_layer": round(ms_step * 1e3 / 7, 3),
+        "decode_tok_s_linear": round(1e3 / (ms_step * n_dec), 1),
         "frac_of_8TBs": round(per_gpu / 8000.0, 4),
         "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(per_gpu / peak, 4), "traffic": None,
-                     "kernel": "sqz::stack_gemv<3> (persistent, fused TP reduce)",
+                     "kernel": "sqz::stack_gemv<3> (persistent" +
+                               (", fused TP reduce)" if world > 1 else ")"),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback",
-                     "algorithmic_bytes_per_step": bytes_step, "per": "GPU"},
-        "e2e": e2e, "clocks": clocks, "gpu_launches": 1, "gemvs_timed": args.steps * len(SHAPES),
+                     "algorithmic_bytes_per_step": bytes_step, "per": "GPU",
+                     "per_gpu_shard_bytes_per_step": shard_bytes},
+        "e2e": e2e, "clocks": clocks, "gpu_launches": 1, "gemvs_timed": args.steps * 7,
         "mode": "stack-tp", "setup_s": round(setup_s, 1),
     }
     print(json.dumps(line), flush=True)
@@ -779,8 +858,13 @@ def main():
                     help="stack: one persistent launch for all K steps; graph: one launch "
                          "per GEMV captured in a CUDA graph")
     ap.add_argument("--rotation", type=int, default=16,
-                    help="decoder layers of distinct device weights (working set >> L2)")
+                    help="decoder layers of distinct device weights (working set >> L2; the "
+                         "TP path sizes its own rotation unless --no-rotation-auto)")
+    ap.add_argument("--no-rotation-auto", dest="rotation_auto", action="store_false")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of load before timing")
+    ap.add_argument("--workload", choices=["auto", "7b", "65b"], default="auto",
+                    help="auto: the LLaMA-7B chain (configs[1]) at N=1, the 65B chain "
+                         "tensor-parallel (configs[3]) at N>1")
     ap.add_argument("--multi", choices=["tp", "replicas"], default="tp",
                     help="N>1: tensor-parallel decoder layers (fused all-reduce) or N replicas")
     ap.add_argument("--force-tp", action="store_true",
@@ -801,7 +885,7 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
-    use_tp = (world > 1 and args.multi == "tp") or args.force_tp
+    use_tp = (world > 1 and args.multi == "tp") or args.force_tp or args.workload == "65b"
     if world > 1 or args.force_tp:
         import torch
         import torch.distributed as dist

@@ -293,6 +293,32 @@ int dsq_cuda_stack_run_host(dsq_cuda_stack* stack, const void* x_host, void* x_d
                             void* stream);
 int dsq_cuda_stack_destroy(dsq_cuda_stack* stack);
 
+/* ---- tensor-parallel sharding (host) ------------------------------
+ * dsq_split_range: [lo, hi) of an even split of n into `world` parts on
+ *   `align` boundaries (the split every rank computes identically).
+ * dsq_shard_rows (column-parallel: q/k/v/gate/up): output rows [lo, hi); the
+ *   rows' packed indices, LUTs and CSR rows move with them.
+ * dsq_shard_cols (row-parallel: o/down): input columns [lo, hi) (align 32
+ *   keeps whole index groups); indices re-packed in the reference LSB-first
+ *   layout (packfmt.cpp:40-53), LUTs replicated, CSR filtered and rebased;
+ *   channel-wise LUTs only (DSQ_E_UNSUPPORTED otherwise).
+ * dsq_shard_decoder: the 7 shards of one decoder layer given in the order
+ *   v, q, o, k, up, gate, down (o and down row-parallel, the rest
+ *   column-parallel), out[7].
+ * A shard owns its arrays; dsq_shard_get returns a view into them (valid
+ * until dsq_shard_destroy) that dsq_cuda_layer_create accepts, and lo/hi. */
+typedef struct dsq_shard dsq_shard;
+int dsq_split_range(uint32_t n, uint32_t world, uint32_t rank, uint32_t align, uint32_t* lo,
+                    uint32_t* hi);
+int dsq_shard_rows(const dsq_layer_view* layer, uint32_t rank, uint32_t world, uint32_t align,
+                   dsq_shard** out);
+int dsq_shard_cols(const dsq_layer_view* layer, uint32_t rank, uint32_t world, uint32_t align,
+                   dsq_shard** out);
+int dsq_shard_decoder(const dsq_layer_view* layers, uint32_t rank, uint32_t world,
+                      uint32_t align, dsq_shard** out);
+int dsq_shard_get(const dsq_shard* shard, dsq_layer_view* view, uint32_t* lo, uint32_t* hi);
+int dsq_shard_destroy(dsq_shard* shard);
+
 /* ---- tensor parallelism: the all-reduce fused into the stack -- */
 /* One context per rank (one process per GPU): a receive buffer for the
  * partial outputs of row-parallel layers ([2][world][max_rows] 64-bit words

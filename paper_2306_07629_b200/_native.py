@@ -137,6 +137,17 @@ PROTOTYPES = {
     "dsq_cuda_dequantize_layer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsq_cuda_dequantize_layer_host": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dsq_cuda_packed_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    "dsq_split_range": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "dsq_shard_rows": (C.c_int, [C.POINTER(LayerView), C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.POINTER(C.c_void_p)]),
+    "dsq_shard_cols": (C.c_int, [C.POINTER(LayerView), C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.POINTER(C.c_void_p)]),
+    "dsq_shard_decoder": (C.c_int, [C.POINTER(LayerView), C.c_uint32, C.c_uint32, C.c_uint32,
+                                    C.POINTER(C.c_void_p)]),
+    "dsq_shard_get": (C.c_int, [C.c_void_p, C.POINTER(LayerView), C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint32)]),
+    "dsq_shard_destroy": (C.c_int, [C.c_void_p]),
     "dsq_cuda_csr_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "dsq_bytes_touched_estimate": (C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                                 C.c_uint64]),

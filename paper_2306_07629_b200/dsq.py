@@ -95,43 +95,52 @@ def _ptr(a: np.ndarray | None) -> int | None:
     return None if a is None else a.ctypes.data
 
 
+def layer_view(layer: QuantizedLayer, keep: list) -> N.LayerView:
+    """The C-ABI view (dsq_layer_view) of a layer; the arrays it points into
+    are appended to `keep` and must outlive the view."""
+    p, s = layer.packed, layer.sparse
+
+    def hold(a, dtype):
+        a = np.ascontiguousarray(a, dtype=dtype)
+        keep.append(a)
+        return a
+
+    luts = hold(p.luts, p.luts.dtype if p.luts.dtype in (np.float16, np.float32) else np.float32)
+    payload = hold(p.payload, np.uint8)
+    row_ptr = hold(s.row_ptr, np.uint32)
+    col_idx = hold(s.col_idx, np.uint16)
+    vals = hold(s.values, s.values.dtype if s.values.dtype in (np.float16, np.float32) else np.float32)
+    v = N.LayerView()
+    name = layer.name.encode()
+    keep.append(name)
+    v.name = name
+    v.rows, v.cols = layer.rows, layer.cols
+    v.packed.bits, v.packed.rows, v.packed.cols = p.bits, p.rows, p.cols
+    v.packed.groups_per_row = p.groups_per_row
+    if luts.dtype == np.float16:
+        v.packed.luts_f16 = _ptr(luts)
+    else:
+        v.packed.luts_f32 = _ptr(luts)
+    v.packed.payload = _ptr(payload)
+    v.packed.payload_len = payload.size
+    v.sparse.rows, v.sparse.cols, v.sparse.nnz = s.rows, s.cols, s.nnz()
+    v.sparse.row_ptr = _ptr(row_ptr)
+    v.sparse.col_idx = _ptr(col_idx) if col_idx.size else None
+    if vals.size:
+        if vals.dtype == np.float16:
+            v.sparse.values_f16 = _ptr(vals)
+        else:
+            v.sparse.values_f32 = _ptr(vals)
+    v.hybrid_top_k = layer.hybrid_top_k
+    return v
+
+
 class DeviceLayer:
     """Owning handle of an uploaded layer (dsq_cuda_layer_create)."""
 
     def __init__(self, layer: QuantizedLayer, device: int = 0):
-        p, s = layer.packed, layer.sparse
         self._keep = []
-
-        def keep(a, dtype):
-            a = np.ascontiguousarray(a, dtype=dtype)
-            self._keep.append(a)
-            return a
-
-        luts = keep(p.luts, p.luts.dtype if p.luts.dtype in (np.float16, np.float32) else np.float32)
-        payload = keep(p.payload, np.uint8)
-        row_ptr = keep(s.row_ptr, np.uint32)
-        col_idx = keep(s.col_idx, np.uint16)
-        vals = keep(s.values, s.values.dtype if s.values.dtype in (np.float16, np.float32) else np.float32)
-        v = N.LayerView()
-        v.name = layer.name.encode()
-        v.rows, v.cols = layer.rows, layer.cols
-        v.packed.bits, v.packed.rows, v.packed.cols = p.bits, p.rows, p.cols
-        v.packed.groups_per_row = p.groups_per_row
-        if luts.dtype == np.float16:
-            v.packed.luts_f16 = _ptr(luts)
-        else:
-            v.packed.luts_f32 = _ptr(luts)
-        v.packed.payload = _ptr(payload)
-        v.packed.payload_len = payload.size
-        v.sparse.rows, v.sparse.cols, v.sparse.nnz = s.rows, s.cols, s.nnz()
-        v.sparse.row_ptr = _ptr(row_ptr)
-        v.sparse.col_idx = _ptr(col_idx) if col_idx.size else None
-        if vals.size:
-            if vals.dtype == np.float16:
-                v.sparse.values_f16 = _ptr(vals)
-            else:
-                v.sparse.values_f32 = _ptr(vals)
-        v.hybrid_top_k = layer.hybrid_top_k
+        v = layer_view(layer, self._keep)
         h = C.c_void_p()
         check(lib.dsq_cuda_layer_create(C.byref(v), device, C.byref(h)))
         self._keep = None

@@ -1,4 +1,5 @@
-"""Tensor-parallel sharding of a quantized layer (host logic).
+"""Tensor-parallel sharding of a quantized layer (host logic, C++ in
+csrc/shard.cpp behind the C ABI dsq_shard_*; this module is its binding).
 
 The product y = D.x + S.x of one layer shards two ways:
 
@@ -18,79 +19,72 @@ owns its column, so every shard's fused product is exact for its slice.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
-from .dsq import CsrMatrix, PackedDense, QuantizedLayer, row_stride
+from . import _native as N
+from ._native import lib
+from .dsq import CsrMatrix, PackedDense, QuantizedLayer, check, layer_view
 
 
 def split_range(n: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:
-    """[lo, hi) of an even split of n into `world` parts on `align` boundaries."""
-    units = (n + align - 1) // align
-    lo = (units * rank) // world * align
-    hi = min(n, (units * (rank + 1)) // world * align)
-    return lo, hi
+    """[lo, hi) of an even split of n into `world` parts on `align` boundaries
+    (dsq_split_range)."""
+    lo, hi = C.c_uint32(), C.c_uint32()
+    check(lib.dsq_split_range(n, world, rank, align, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
-def _unpack_rows(p: PackedDense) -> np.ndarray:
-    """Reference-layout payload -> indices [rows, cols] (vectorised unpack,
-    packfmt.cpp:57-80 semantics)."""
-    stride = p.row_stride()
-    raw = np.asarray(p.payload, np.uint8).reshape(p.rows, stride)
-    bits = np.unpackbits(raw, axis=1, bitorder="little")[:, : p.cols * p.bits]
-    bits = bits.reshape(p.rows, p.cols, p.bits).astype(np.uint16)
-    weights = (1 << np.arange(p.bits, dtype=np.uint16))
-    return (bits * weights).sum(axis=2).astype(np.uint16)
+def _from_shard(h) -> tuple[QuantizedLayer, int, int]:
+    """Copy a dsq_shard's arrays into a QuantizedLayer, then free the shard."""
+    try:
+        v, lo, hi = N.LayerView(), C.c_uint32(), C.c_uint32()
+        check(lib.dsq_shard_get(h, C.byref(v), C.byref(lo), C.byref(hi)))
+        p, sp = v.packed, v.sparse
+        k = (1 << p.bits) * p.groups_per_row
 
+        def arr(ptr, n, dtype):
+            if not ptr or n == 0:
+                return np.zeros(0, dtype)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dtype))),
+                                         shape=(n,)).copy()
 
-def _pack_rows(idx: np.ndarray, bits: int) -> np.ndarray:
-    """indices [rows, cols] -> reference-layout payload (packfmt.cpp:18-55)."""
-    rows, cols = idx.shape
-    b = ((idx[:, :, None] >> np.arange(bits, dtype=np.uint16)) & 1).astype(np.uint8)
-    b = b.reshape(rows, cols * bits)
-    stride = row_stride(cols, bits)
-    pad = stride * 8 - cols * bits
-    if pad:
-        b = np.concatenate([b, np.zeros((rows, pad), np.uint8)], axis=1)
-    return np.packbits(b, axis=1, bitorder="little").reshape(-1)
+        luts = (arr(p.luts_f16, p.rows * k, np.uint16).view(np.float16) if p.luts_f16
+                else arr(p.luts_f32, p.rows * k, np.float32))
+        payload = arr(p.payload, p.payload_len, np.uint8)
+        row_ptr = arr(sp.row_ptr, sp.rows + 1, np.uint32)
+        col_idx = arr(sp.col_idx, sp.nnz, np.uint16)
+        vals = (arr(sp.values_f16, sp.nnz, np.uint16).view(np.float16) if sp.values_f16
+                else arr(sp.values_f32, sp.nnz, np.float32))
+        q = QuantizedLayer(v.name.decode(), v.rows, v.cols,
+                           PackedDense(p.bits, p.rows, p.cols, luts, payload, p.groups_per_row),
+                           CsrMatrix(sp.rows, sp.cols, row_ptr, col_idx, vals), v.hybrid_top_k)
+        return q, lo.value, hi.value
+    finally:
+        lib.dsq_shard_destroy(h)
 
 
 def shard_rows(layer: QuantizedLayer, rank: int, world: int,
                align: int = 1) -> tuple[QuantizedLayer, int, int]:
-    """Column-parallel shard: output rows [r0, r1)."""
-    p, s = layer.packed, layer.sparse
-    r0, r1 = split_range(layer.rows, world, rank, align)
-    k = p.levels() * p.groups_per_row
-    stride = p.row_stride()
-    a, b = int(s.row_ptr[r0]), int(s.row_ptr[r1])
-    packed = PackedDense(p.bits, r1 - r0, p.cols, np.asarray(p.luts)[r0 * k:r1 * k],
-                         np.asarray(p.payload)[r0 * stride:r1 * stride], p.groups_per_row)
-    sparse = CsrMatrix(r1 - r0, s.cols, (np.asarray(s.row_ptr[r0:r1 + 1]) - a).astype(np.uint32),
-                       np.asarray(s.col_idx)[a:b], np.asarray(s.values)[a:b])
-    return (QuantizedLayer(f"{layer.name}.r{rank}", r1 - r0, layer.cols, packed, sparse,
-                           min(layer.hybrid_top_k, r1 - r0)), r0, r1)
+    """Column-parallel shard: output rows [r0, r1) (dsq_shard_rows)."""
+    keep: list = []
+    v = layer_view(layer, keep)
+    h = C.c_void_p()
+    check(lib.dsq_shard_rows(C.byref(v), rank, world, align, C.byref(h)))
+    return _from_shard(h)
 
 
 def shard_cols(layer: QuantizedLayer, rank: int, world: int,
                align: int = 32) -> tuple[QuantizedLayer, int, int]:
-    """Row-parallel shard: input columns [c0, c1) (align-column boundaries)."""
-    p, s = layer.packed, layer.sparse
-    if p.groups_per_row != 1:
-        raise ValueError("row-parallel sharding implemented for channel-wise LUTs")
-    c0, c1 = split_range(layer.cols, world, rank, align)
-    idx = _unpack_rows(p)[:, c0:c1]
-    packed = PackedDense(p.bits, p.rows, c1 - c0, np.asarray(p.luts),
-                         _pack_rows(idx, p.bits), 1)
-    rp = np.asarray(s.row_ptr, np.int64)
-    ci = np.asarray(s.col_idx, np.int64)
-    keep = (ci >= c0) & (ci < c1)
-    rows_of = np.repeat(np.arange(layer.rows), np.diff(rp))
-    new_rp = np.zeros(layer.rows + 1, np.int64)
-    np.add.at(new_rp, rows_of[keep] + 1, 1)
-    new_rp = np.cumsum(new_rp).astype(np.uint32)
-    sparse = CsrMatrix(layer.rows, c1 - c0, new_rp, (ci[keep] - c0).astype(np.uint16),
-                       np.asarray(s.values)[keep])
-    return (QuantizedLayer(f"{layer.name}.c{rank}", layer.rows, c1 - c0, packed, sparse,
-                           layer.hybrid_top_k), c0, c1)
+    """Row-parallel shard: input columns [c0, c1) (dsq_shard_cols: indices
+    re-packed in the reference LSB-first layout, LUTs replicated, CSR filtered
+    and rebased)."""
+    keep: list = []
+    v = layer_view(layer, keep)
+    h = C.c_void_p()
+    check(lib.dsq_shard_cols(C.byref(v), rank, world, align, C.byref(h)))
+    return _from_shard(h)
 
 
 # ---------------------------------------------------------------------------
@@ -108,16 +102,15 @@ CHAIN_IN = [-1, -1, 0, -1, 2, 2, 4]  # input of each GEMV within a step (bench.p
 
 
 def shard_decoder(layers: list, rank: int, world: int, align: int = 32) -> list:
-    """The 7 shards (QuantizedLayer) of one decoder layer for `rank`."""
-    out = []
-    for name, q in zip(DECODER, layers):
-        if world == 1:
-            out.append(q)
-        elif name in ROW_PARALLEL:
-            out.append(shard_cols(q, rank, world, align)[0])
-        else:
-            out.append(shard_rows(q, rank, world, align)[0])
-    return out
+    """The 7 shards (QuantizedLayer) of one decoder layer for `rank`
+    (dsq_shard_decoder; layers in DECODER order)."""
+    if world == 1:
+        return list(layers)
+    keep: list = []
+    views = (N.LayerView * 7)(*[layer_view(q, keep) for q in layers])
+    hs = (C.c_void_p * 7)()
+    check(lib.dsq_shard_decoder(views, rank, world, align, hs))
+    return [_from_shard(C.c_void_p(h))[0] for h in hs]
 
 
 def decoder_chain(n_steps: int, slots: int, first_x: bool = True):

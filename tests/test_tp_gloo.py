@@ -144,3 +144,43 @@ def test_decoder_shards_chain_locally():
     assert deps[:7] == [-1, -1, 0, -1, 2, 2, 4] and deps[7:14] == [6, 6, 7, 6, 9, 9, 11]
     assert [reduce[i] for i in range(7)] == [n in ("o", "down") for n in DECODER]
     assert [i for i, r in enumerate(reduce) if r] == [2, 6, 9, 13]
+
+
+@pytest.mark.parametrize("bits,rows,cols,world", [(3, 40, 200, 2), (4, 33, 320, 3), (2, 17, 96, 4),
+                                                  (5, 8, 250, 2), (8, 9, 64, 2)])
+def test_shard_cols_repack_matches_oracle(oracle, bits, rows, cols, world):
+    """dsq_shard_cols (C++) re-packs each column slice exactly like the
+    reference pack() of the sliced indices; CSR entries filtered and rebased."""
+    from paper_2306_07629_b200.tp import shard_cols, shard_rows, split_range
+    L = make_layer(rows, cols, bits, 0.05, seed=rows * bits + cols, skew="zipf")
+    q = to_quantized_layer(L)
+    rc, assign = oracle.unpack(L.payload, bits, rows, cols)
+    assert rc == 0
+    idx = assign.reshape(rows, cols)
+    for rank in range(world):
+        sq, c0, c1 = shard_cols(q, rank, world, 8)
+        assert (c0, c1) == split_range(cols, world, rank, 8)
+        want = oracle.pack(np.ascontiguousarray(idx[:, c0:c1]).reshape(-1), bits, rows, c1 - c0)
+        assert np.array_equal(np.asarray(sq.packed.payload), want)
+        keep = (L.col_idx >= c0) & (L.col_idx < c1)
+        assert np.array_equal(np.asarray(sq.sparse.col_idx), (L.col_idx[keep] - c0).astype(np.uint16))
+        assert np.array_equal(np.asarray(sq.sparse.values), L.values16[keep])
+        sr, r0, r1 = shard_rows(q, rank, world)
+        assert np.array_equal(np.asarray(sr.packed.luts), L.luts16[r0 * (1 << bits):r1 * (1 << bits)])
+
+
+def test_shard_decoder_roles():
+    """v,q,k,up,gate split by rows, o and down by 32-aligned columns."""
+    from paper_2306_07629_b200.tp import shard_decoder, split_range
+    shapes = [(64, 96), (64, 96), (96, 64), (64, 96), (160, 96), (160, 96), (96, 160)]
+    qs = [to_quantized_layer(make_layer(r, c, 3, 0.01, seed=i), name=f"l{i}")
+          for i, (r, c) in enumerate(shapes)]
+    for rank in range(2):
+        out = shard_decoder(qs, rank, 2)
+        for i, ((r, c), s) in enumerate(zip(shapes, out)):
+            if i in (2, 6):
+                lo, hi = split_range(c, 2, rank, 32)
+                assert (s.rows, s.cols) == (r, hi - lo) and s.name.endswith(f".c{rank}")
+            else:
+                lo, hi = split_range(r, 2, rank, 32)
+                assert (s.rows, s.cols) == (hi - lo, c) and s.name.endswith(f".r{rank}")
