@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <immintrin.h>
+
 #include "../../include/dsq_cuda.h"
 #include "layout.hpp"
 #include "stack.hpp"
@@ -340,6 +342,9 @@ struct dsq_cuda_layer {
     float* y32 = nullptr;       // host-API output staging
     float* x32 = nullptr;       // host-API input staging
     float* x32_pin = nullptr;   // host-API pinned, device-mapped staging (lazy)
+    uint16_t* x16_pin = nullptr;  // host-API: fp16 x converted on the host (F16C)
+    uint16_t* x16_map = nullptr;
+    cudaGraphExec_t host_graph[4] = {nullptr, nullptr, nullptr, nullptr};  // per kernel
     float* y32_pin = nullptr;
     float* x32_map = nullptr;   // their device addresses
     float* y32_map = nullptr;
@@ -760,8 +765,11 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
 int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (!L) return DSQ_OK;
     cudaSetDevice(L->device);
+    for (auto& g : L->host_graph)
+        if (g) cudaGraphExecDestroy(g);
     if (L->stream) cudaStreamDestroy(L->stream);
     if (L->x32_pin) cudaFreeHost(L->x32_pin);
+    if (L->x16_pin) cudaFreeHost(L->x16_pin);
     if (L->y32_pin) cudaFreeHost(L->y32_pin);
     if (L->dense_w) cudaFree(L->dense_w);
     if (L->batch_part) cudaFree(L->batch_part);
@@ -989,37 +997,108 @@ int dsq_cuda_dense_gemv(const uint16_t* w, uint32_t rows, uint32_t cols, const v
     return DSQ_OK;
 }
 
+// host-side conversions of the reference-signature call: fp32 -> fp16
+// (round to nearest even, like __float2half_rn) with F16C, fp32 -> fp64 with
+// AVX; scalar fallbacks on CPUs without them
+__attribute__((target("avx,f16c"))) static void f32_to_f16_f16c(const float* in, uint16_t* out,
+                                                                size_t n) {
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8)
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(out + i),
+                         _mm256_cvtps_ph(_mm256_loadu_ps(in + i), _MM_FROUND_TO_NEAREST_INT));
+    for (; i < n; ++i) out[i] = f32_to_f16(in[i]);
+}
+__attribute__((target("avx"))) static void f32_to_f64_avx(const float* in, double* out,
+                                                          size_t n) {
+    size_t i = 0;
+    for (; i + 4 <= n; i += 4) _mm256_storeu_pd(out + i, _mm256_cvtps_pd(_mm_loadu_ps(in + i)));
+    for (; i < n; ++i) out[i] = double(in[i]);
+}
+static void host_x_to_f16(const float* in, uint16_t* out, size_t n) {
+    static const bool f16c = __builtin_cpu_supports("f16c") && __builtin_cpu_supports("avx");
+    if (f16c) {
+        f32_to_f16_f16c(in, out, n);
+    } else {
+        for (size_t i = 0; i < n; ++i) out[i] = f32_to_f16(in[i]);
+    }
+}
+static void host_y_to_f64(const float* in, double* out, size_t n) {
+    static const bool avx = __builtin_cpu_supports("avx");
+    if (avx) {
+        f32_to_f64_avx(in, out, n);
+    } else {
+        for (size_t i = 0; i < n; ++i) out[i] = double(in[i]);
+    }
+}
+
+// The reference-signature product (fp32 host x -> fp64 host y): x is
+// converted to fp16 on the host straight into pinned, device-mapped staging;
+// one captured CUDA graph per kernel replays "pinned x16 -> device x16 (one
+// small PDL copy kernel) -> the product, y written as fp32 straight into
+// pinned, device-mapped host memory"; then one stream synchronisation and a
+// vectorised fp64 widen.  (The x / y buffers are the layer's own, so the
+// graph is captured once and replayed.)
 int dsq_cuda_matvec_host(const dsq_cuda_layer* Lc, int kernel, const float* x_host,
                          double* y_host) {
     auto* L = const_cast<dsq_cuda_layer*>(Lc);
     if (!L || !x_host || !y_host) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
+    if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)
+        return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);
     cudaSetDevice(L->device);
     std::lock_guard<std::mutex> lk(L->host_mu);
-    // pinned, device-mapped staging: the fp32 -> fp16 kernel reads x over
-    // PCIe and the product writes y straight into host memory, so a call is
-    // two launches (the second overlapping the first under PDL) and one
-    // synchronisation, no copy-engine transfers
-    if (!L->x32_pin) {
+    const size_t x16_bytes = (size_t(L->cols) * 2 + 15) / 16 * 16;
+    if (!L->x16_pin) {
         const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
-        cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&L->x32_pin), size_t(L->cols) * 4, fl);
-        if (e == cudaSuccess)
+        cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&L->x16_pin), x16_bytes, fl);
+        if (e == cudaSuccess && !L->y32_pin)
             e = cudaHostAlloc(reinterpret_cast<void**>(&L->y32_pin), size_t(L->rows) * 4, fl);
         if (e == cudaSuccess)
-            e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->x32_map), L->x32_pin, 0);
+            e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->x16_map), L->x16_pin, 0);
         if (e == cudaSuccess)
             e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->y32_map), L->y32_pin, 0);
         if (e != cudaSuccess) {
-            if (L->x32_pin) cudaFreeHost(L->x32_pin);
+            if (L->x16_pin) cudaFreeHost(L->x16_pin);
             if (L->y32_pin) cudaFreeHost(L->y32_pin);
-            L->x32_pin = L->y32_pin = L->x32_map = L->y32_map = nullptr;
+            L->x16_pin = nullptr;
+            L->y32_pin = nullptr;
+            L->x16_map = nullptr;
+            L->y32_map = nullptr;
             return cuda_fail(e, "host-API staging");
         }
+        std::memset(L->x16_pin, 0, x16_bytes);
     }
-    std::memcpy(L->x32_pin, x_host, size_t(L->cols) * 4);
-    int rc = gemv_impl(L, kernel, L->x32_map, DSQ_F32, L->y32_map, DSQ_F32, 1, L->stream, true);
-    if (rc) return rc;
+    cudaGraphExec_t& g = L->host_graph[kernel];
+    if (!g) {
+        if (kernel == DSQ_KERNEL_REFERENCE) {  // allocation must precede the capture
+            int rc = ensure_dense(L, L->stream);
+            if (rc) return rc;
+            CUDA_TRY(cudaStreamSynchronize(L->stream));
+        }
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(L->stream, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = launch_upload_x(L->x16_map, L->x16, x16_bytes, L->stream);
+        int rc = e == cudaSuccess ? gemv_impl(L, kernel, L->x16, DSQ_F16, L->y32_map, DSQ_F32, 1,
+                                              L->stream, true)
+                                  : DSQ_OK;
+        cudaError_t e2 = cudaStreamEndCapture(L->stream, &graph);
+        if (e != cudaSuccess) return cuda_fail(e, "host-API graph capture (upload)");
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e2 != cudaSuccess) return cuda_fail(e2, "host-API graph capture");
+        e = cudaGraphInstantiate(&g, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            g = nullptr;
+            return cuda_fail(e, "host-API graph instantiate");
+        }
+    }
+    host_x_to_f16(x_host, L->x16_pin, L->cols);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    CUDA_TRY(cudaGraphLaunch(g, L->stream));
     CUDA_TRY(cudaStreamSynchronize(L->stream));
-    for (uint32_t r = 0; r < L->rows; ++r) y_host[r] = double(L->y32_pin[r]);
+    host_y_to_f64(L->y32_pin, y_host, L->rows);
     return DSQ_OK;
 }
 

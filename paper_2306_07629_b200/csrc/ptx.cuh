@@ -360,8 +360,10 @@ __device__ __forceinline__ uint16_t ld_cg_u16(const uint16_t* p) {
     asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(r) : "l"(p));
     return r;
 }
+// named barrier among a subset of warps; the non-.aligned form, so the
+// warps may reach it from different code paths / convergence states
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 }  // namespace sqz

@@ -86,6 +86,11 @@ __device__ __forceinline__ Share cta_share(const StackLayerDesc& d, uint32_t cta
 // dev-only experiment switches (StackParams::dbg bits 1 / 8 skip the decode
 // math / the weight loads): compiled in only with -DDSQ_STACK_DEV (the
 // variant-lib / profile builds), so the product library can never skip work
+#ifdef DSQ_MULTI_SIGNAL  // dev comparison: one release per finishing warp
+constexpr bool kOneSignal = false;
+#else
+constexpr bool kOneSignal = true;
+#endif
 #if defined(DSQ_STACK_DEV) || defined(DSQ_STACK_PROFILE)
 constexpr bool kDevSwitches = true;
 #else
@@ -115,6 +120,7 @@ __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int li
 }
 #define mbar_wait(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
 #define mbar_wait_cons(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
+#define mbar_wait_edge(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
 #define mbar_wait_role(bar, parity, ns) mbar_wait_wd(bar, parity, __LINE__)
 #define mbar_wait_fin(bar, parity) mbar_wait_wd(bar, parity, __LINE__)
 #define DSQ_WD_POLL(cond, ...)                                \
@@ -136,6 +142,16 @@ __device__ __noinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int li
 #else
 #define mbar_wait_cons(bar, parity) mbar_wait(bar, parity)
 #endif
+// decode warps at a layer start (x staged, partial buffer free): the
+// suspend-hint wait, or with DSQ_EDGE_SLEEP=ns a probe + plain nanosleep
+#ifndef DSQ_EDGE_SLEEP
+#define DSQ_EDGE_SLEEP 0
+#endif
+#define mbar_wait_edge(bar, parity)                                         \
+    do {                                                                    \
+        if (DSQ_EDGE_SLEEP) mbar_wait_sleep(bar, parity, DSQ_EDGE_SLEEP);    \
+        else mbar_wait(bar, parity);                                        \
+    } while (0)
 // role-warp waits (publisher / loader: off the critical path; finishing and
 // CSR warps: DSQ_FIN_SLEEP ns, 0 = the suspend-hint wait)
 #ifndef DSQ_ROLE_SLEEP
@@ -245,6 +261,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     uint8_t* ring = sm + p.off_ring;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t cta = blockIdx.x, G = p.grid;
+    // completion signals per CTA and layer (the dependency target is G x this)
+    const uint32_t sig_per_cta = kOneSignal ? 1u : 1u + p.csr_warps;
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < NC * WS; ++s) mbar_init(&full[s], 1);
@@ -427,7 +445,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             }
             if (d.dep != kNoDep) {
                 if (lane == 0) {
-                    DSQ_WD_POLL(ld_acquire_gpu(p.counters + d.dep) < G * (1 + p.csr_warps),
+                    DSQ_WD_POLL(ld_acquire_gpu(p.counters + d.dep) < G * sig_per_cta,
                                 "stack watchdog: cta %u layer %u dep %u counter %u\n", cta, l, d.dep,
                                 *(volatile const uint32_t*)(p.counters + d.dep));
                     DSQ_TRACE(l, kTrDepMet);
@@ -557,14 +575,21 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             if (f == 0) DSQ_TRACE(l, kTrFinalDone);
             mbar_arrive(&pempty[b]);
             mbar_arrive(&bempty[b]);
-            red_release_gpu_add(p.counters + l, 1u);
-            if (f == 0) DSQ_TRACE(l, kTrSignaled);
+            if (!kOneSignal) red_release_gpu_add(p.counters + l, 1u);
         }
+        if (kOneSignal) {
+            // the CTA's finishing warps meet (CTA-scope ordering of all their
+            // y stores), then ONE release per CTA: 148 same-address atomics
+            // per layer instead of 148 x (1 + csr_warps)
+            named_bar_sync(2, 32 * kFin);
+            if (f == 0 && lane == 0) red_release_gpu_add(p.counters + l, 1u);
+        }
+        if (f == 0 && lane == 0) DSQ_TRACE(l, kTrSignaled);
         if (notify && f == 0 && cta == 0) {
             // every finishing warp of every CTA is done: copy step `notify`'s
             // output to the host (one burst of PCIe writes), then announce it
             if (lane == 0)
-                while (ld_acquire_gpu(p.counters + l) < G * (1 + p.csr_warps)) __nanosleep(32);
+                while (ld_acquire_gpu(p.counters + l) < G * sig_per_cta) __nanosleep(32);
             __syncwarp();
             const uint32_t n16 = p.serve_y_bytes / 16;
             const uint4* ysrc = static_cast<const uint4*>(d.y);
@@ -592,6 +617,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     // the last finishing warp of the last CTA resets the counters for the
     // next launch (all finishing warps of a CTA meet at named barrier 1)
     auto finish_kernel = [&]() {
+        __syncwarp();  // bar.sync is .aligned: the warp must arrive converged
+                       // (desc_release's lane-0 arrive diverged it; synccheck)
         named_bar_sync(1, 32 * kFin);
         if (warp == NC + 2 && lane == 0) {
             const uint32_t old = atomicAdd(p.counters + p.n_layers, 1u);
@@ -738,8 +765,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         const uint32_t NS = d.ns, cu = d.cu;
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrConsStart);
         DSQ_LAP(c_top);
-        mbar_wait_cons(&xfull[b], (l >> 1) & 1u);
-        if (l >= 2) mbar_wait_cons(&pempty[b], ((l >> 1) - 1) & 1u);
+        mbar_wait_edge(&xfull[b], (l >> 1) & 1u);
+        if (l >= 2) mbar_wait_edge(&pempty[b], ((l >> 1) - 1) & 1u);
         DSQ_LAP(c_xw);
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrXReady);
         const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);

@@ -6,6 +6,9 @@
 // Built here against /root/reference/proj/include + oracle/_ref/libdsqref.so
 // (make cxx-test); the binary travels to the GPU box and is run by
 // tests/test_cxx_wrapper.py (GPU).  Exit code 0 = pass.
+#include <omp.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <vector>
@@ -153,6 +156,50 @@ int main() {
                 return fail("codebook", double(g));
         std::printf("decompose + quantize_channelwise: bit-identical (%u extracted)\n",
                     dr.sparse.row_ptr.back());
+    } catch (const sqz::Error& e) {
+        std::printf("sqz::Error status %d: %s\n", e.status(), e.what());
+        return 2;
+    }
+    // the reference-signature call at LLaMA-7B shapes (the cmd_matvec path):
+    // wall time per product, our host call vs the reference on the host cores
+    try {
+        for (uint32_t rc2 : {4096u, 11008u}) {
+            const uint32_t R = rc2, Cc = 4096;
+            Rng r2(11);
+            AssignmentVector as(size_t(R) * Cc);
+            for (auto& a : as) a = uint16_t(r2.below(8));
+            std::vector<Codebook> cbs(R);
+            for (auto& cb : cbs) {
+                cb.centroids.resize(8);
+                for (auto& c : cb.centroids) c = round_f16(float(r2.normal()) * 0.02f);
+                std::sort(cb.centroids.begin(), cb.centroids.end());
+            }
+            QuantizedLayer big;
+            big.name = "big";
+            big.rows = R;
+            big.cols = Cc;
+            big.packed = pack(as, cbs, 3, R, Cc);
+            std::vector<uint32_t> tr, tc;
+            std::vector<float> tv;
+            for (uint32_t r = 0; r < R; ++r)
+                for (uint32_t c = r % 223; c < Cc; c += 223) {  // ~0.45%
+                    tr.push_back(r);
+                    tc.push_back(c);
+                    tv.push_back(round_f16(float(r2.normal()) * 0.2f));
+                }
+            big.sparse = csr_from_triplets(R, Cc, tr, tc, tv);
+            big.hybrid_top_k = 10;
+            big.hybrid = hybrid_split(big.sparse, 10);
+            std::vector<float> xb(Cc);
+            for (auto& v : xb) v = round_f16(float(r2.normal()));
+            const sqz::BenchRecord g = sqz::bench_matvec(big, xb, 51, BenchKernel::fused);
+            const BenchRecord rr = bench_matvec(big, xb, 5, BenchKernel::fused, Exec::parallel);
+            const double e = normwise(sqz::DeviceLayer(big).fused(xb), fused_dns_matvec(big, xb));
+            std::printf("host call %ux%u fused: %.1f us per product (reference %.0f us, %d threads),"
+                        " normwise err %.2e\n", R, Cc, g.median_seconds * 1e6,
+                        rr.median_seconds * 1e6, omp_get_max_threads(), e);
+            if (e > 1e-5) return fail("host call at 7B shape", e);
+        }
     } catch (const sqz::Error& e) {
         std::printf("sqz::Error status %d: %s\n", e.status(), e.what());
         return 2;

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../paper_2306_07629_b200/csrc/tile.cuh"
 
@@ -566,7 +567,99 @@ __global__ void __launch_bounds__(1024, 1) k_layers_ldg(const uint32_t* __restri
     out[blockIdx.x * blockDim.x + threadIdx.x] = part[lane] + float(cur[0] & 1);
 }
 
-int main() {
+// V10: V8 with one flat pair loop per layer -- the tile change is a rare
+// uniform branch inside the loop (no segment restarts), accumulators d0/d1
+// alternate by unit parity and are flushed together
+__global__ void __launch_bounds__(1024, 1) k_flat(const uint32_t* __restrict__ g, int L, int U,
+                                                  int NS, int consumers, float* out, ShiftK K,
+                                                  long long* clk, int mode = 0) {
+    extern __shared__ __align__(1024) uint8_t smb[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smb);
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smb + 2048);
+    float* part = reinterpret_cast<float*>(smb + 2048 + 64 * 256 * 2);
+    uint32_t* luts = reinterpret_cast<uint32_t*>(smb + 2048 + 64 * 512 + 16 * 1024);
+    uint8_t* ring = smb + 2048 + 64 * 512 + 16 * 1024 + 4096;
+    const uint32_t slot_bytes = ((U * 384 + 127) / 128) * 128;
+    for (uint32_t i = threadIdx.x; i < 64 * 256; i += blockDim.x) xs[i] = uint16_t(0x3800 + (i & 0x3ff));
+    for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) luts[i] = 0x3c3a3836u ^ i;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < consumers * 2; ++i) mbar_init(&full[i], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (int(warp) >= consumers) return;
+    const uint64_t pol = policy_evict_first();
+    const size_t wbase = (size_t(blockIdx.x) * consumers + warp) * size_t(L) * U * 96;
+    auto issue = [&](int l) {
+        if (l >= L || ((mode & 4) && l >= 2)) return;
+        if (lane == 0) {
+            uint64_t* bar = &full[warp * 2 + (l & 1)];
+            mbar_arrive_expect_tx(bar, U * 384);
+            bulk_g2s(ring + size_t(warp * 2 + (l & 1)) * slot_bytes, g + wbase + size_t(l) * U * 96,
+                     U * 384, bar, pol);
+        }
+    };
+    issue(0);
+    issue(1);
+    const ShiftK k = K;
+    const uint32_t xoff = tile_x_offset(lane), trow = (lane >> 2) & 3u;
+    const uint32_t s_start = (warp * U) % NS, t_start = (warp * U) / NS;
+    long long c0 = clock64();
+    float d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
+    for (int l = 0; l < L; ++l) {
+        if (!(mode & 4) || l < 2) mbar_wait(&full[warp * 2 + (l & 1)], (l >> 1) & 1u);
+        const uint32_t* sp = reinterpret_cast<const uint32_t*>(ring + size_t(warp * 2 + (l & 1)) * slot_bytes) + lane;
+        const uint16_t* xh = xs + (l & 3) * 4096 + xoff;
+        uint32_t s = s_start, tile = t_start;
+        uint4 q0 = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
+        Planes8 P{q0.x, q0.y, q0.z, q0.w};
+        auto flush = [&]() {
+            const float v = tile_rows_reduce(d0, d1, lane);
+            if ((lane & 3) == 0 && lane < 16) part[warp * 256 + ((tile * 4 + trow) & 255)] += v;
+#pragma unroll
+            for (int z = 0; z < 4; ++z) d0[z] = d1[z] = 0.f;
+        };
+        auto next_tile = [&]() {
+            flush();
+            ++tile;
+            s = 0;
+            const uint4 q = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
+            P = Planes8{q.x, q.y, q.z, q.w};
+        };
+        int u = 0;
+#pragma unroll 1
+        for (; u + 1 < U; u += 2) {
+            const uint32_t a0 = sp[0], a1 = sp[32], a2 = sp[64];
+            const uint32_t b0 = sp[96], b1 = sp[128], b2 = sp[160];
+            sp += 192;
+            if (s == uint32_t(NS)) next_tile();
+            const uint16_t* xa = xh + (s & 15) * 256;
+            const uint4 xa0 = ldx(xa, 0), xb0 = ldx(xa, 128);
+            span3_mma_one(a0, a1, a2, P, xa0, xb0, d0, k);
+            ++s;
+            if (s == uint32_t(NS)) next_tile();
+            const uint16_t* xb = xh + (s & 15) * 256;
+            const uint4 xa1 = ldx(xb, 0), xb1 = ldx(xb, 128);
+            span3_mma_one(b0, b1, b2, P, xa1, xb1, d1, k);
+            ++s;
+        }
+        if (u < U) {
+            if (s == uint32_t(NS)) next_tile();
+            const uint16_t* xa = xh + (s & 15) * 256;
+            const uint4 xa0 = ldx(xa, 0), xb0 = ldx(xa, 128);
+            span3_mma_one(sp[0], sp[32], sp[64], P, xa0, xb0, d0, k);
+        }
+        if (!(mode & 2)) flush();
+        __syncwarp();
+        issue(l + 2);
+    }
+    long long c1 = clock64();
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(clk), c1 - c0);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = part[lane] + d0[0] + d1[1];
+}
+
+int main(int argc, char** argv) {
     cudaDeviceProp pr;
     CK(cudaGetDeviceProperties(&pr, 0));
     const int nsm = pr.multiProcessorCount;
@@ -643,32 +736,42 @@ int main() {
             ldg(k_ldg<4>, "V7 ldg D=4 pairs", c);
             ldg(k_ldg<6>, "V7 ldg D=6 pairs", c);
         }
-        auto lay = [&](int c, int U, int NS, bool use_ldg = false, int mode = 0) -> int {
+        auto lay = [&](int c, int U, int NS, bool use_ldg = false, int mode = 0, bool flat = false) -> int {
             const int L = int(total_units / nsm / c / U);
             const size_t smem = 2048 + 64 * 512 + 16 * 1024 + 4096 + size_t(c) * 2 * (((U * 384 + 127) / 128) * 128);
             if (smem > 227 * 1024) return 0;
+            CK(cudaFuncSetAttribute(k_flat, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             if (use_ldg) CK(cudaFuncSetAttribute(k_layers_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             else CK(cudaFuncSetAttribute(k_layers, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk);
+            if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
+            else if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk);
             else k_layers<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
             CK(cudaDeviceSynchronize());
             cudaEventRecord(e0);
-            if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk);
+            if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
+            else if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk);
             else k_layers<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
             cudaEventRecord(e1);
             CK(cudaDeviceSynchronize());
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
             const double w = double(nsm) * c * L * U * 1024.0;
-            printf("mode %d ", mode);
+            printf("%s mode %d ", flat ? "FLAT" : "seg ", mode);
             printf(use_ldg ? "V9 ldg    c%2d U %3d NS %2d: %.3f ms  %6.1f w/clk/SM @1.965  %6.0f GB/s  %.0f ns/layer\n" : "V8 layers c%2d U %3d NS %2d: %.3f ms  %6.1f w/clk/SM @1.965  %6.0f GB/s  %.0f ns/layer\n", c, U, NS,
                    ms, w / (ms * 1e-3) / nsm / 1.965e9, w * 0.375 / (ms * 1e-3) / 1e9, ms * 1e6 / L);
             return 0;
         };
-        for (int mode : {0, 1, 2, 3, 4, 7}) lay(8, 14, 16, false, mode);
-        for (int mode : {0, 4, 7}) lay(8, 28, 16, false, mode);
-        for (int mode : {0, 4, 7}) lay(16, 14, 16, false, mode);
-        lay(8, 14, 16);   // 7B 4096x4096, 8 consumers
+        if (argc > 1) {  // one configuration: c U NS mode flat
+            lay(atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), false, atoi(argv[4]), atoi(argv[5]) != 0);
+            return 0;
+        }
+        for (int flat = 0; flat < 2; ++flat) {
+            for (int mode : {0, 4, 6}) lay(8, 14, 16, false, mode, flat);
+            for (int mode : {0, 6}) lay(8, 28, 16, false, mode, flat);
+            for (int mode : {0, 6}) lay(8, 37, 16, false, mode, flat);
+            for (int mode : {0, 6}) lay(16, 7, 16, false, mode, flat);
+            for (int mode : {0, 6}) lay(16, 19, 16, false, mode, flat);
+        }
         lay(8, 37, 16);   // 7B 11008x4096
         lay(8, 38, 43);   // 7B 4096x11008
         lay(16, 7, 16);
