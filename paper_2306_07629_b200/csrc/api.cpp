@@ -209,8 +209,19 @@ uint32_t max_nnz_per_cta(const std::vector<uint32_t>& rp, uint32_t rows, int G) 
     return m;
 }
 
+constexpr uint64_t kSmallLayerUnits = 200;  // units per CTA below which 8 warps do a layer
+
+// dev (DSQ_STACK_NCA=1): 16-warp stacks whose small layers run on 8 of the
+// warps -- measured slower than an 8-warp kernel on the LLaMA-7B chain (2163
+// vs 2328 GB/s) and the 13B stack, so the default keeps one count per stack
+bool per_layer_nca_enabled() {
+    if (const char* e = std::getenv("DSQ_STACK_NCA")) return atoi(e) != 0;
+    return false;
+}
+
 void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, uint32_t bits,
-               int G) {
+               int G, uint32_t consumers) {
+    static const bool per_layer_nca = per_layer_nca_enabled();
     d.tq = l.tiles / uint32_t(G);
     d.tr = l.tiles % uint32_t(G);
     d.rows = l.rows;
@@ -220,8 +231,15 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, 
     d.cu = slot_bytes / (unit_words(bits) * 4);
     d.dep = kNoDep;
     d.reduce_ord = kNoDep;
-    d.nch_lo = ceil_div(uint64_t(d.tq) * l.ns, d.cu);
-    d.nch_hi = ceil_div(uint64_t(d.tq + 1) * l.ns, d.cu);
+    d.nca = consumers;
+    d.nca_shift = consumers == 16 ? 4u : consumers == 8 ? 3u : 2u;
+    // (dev, DSQ_STACK_NCA=1) a layer that gives a CTA few units runs on the
+    // first 8 of 16 consumer warps
+    const uint64_t units = uint64_t(ceil_div(l.tiles, G)) * l.ns;
+    if (consumers == 16 && units <= kSmallLayerUnits && per_layer_nca) {
+        d.nca = 8;
+        d.nca_shift = 3;
+    }
 }
 
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
@@ -234,9 +252,17 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     // whose layers give a CTA few units (LLaMA-7B 4096-row layers: ~111) run
     // better with 8 consumer warps (twice the units each), big layers with 16
     {
-        uint64_t units = 0;
-        for (uint32_t i = 0; i < n; ++i) units += uint64_t(ceil_div(Ls[i].tiles, G)) * Ls[i].ns;
-        sp.consumers = units <= 200ull * n ? 8u : kStackConsumersDefault;
+        // 16 warps when any layer is large (the small ones then run on 8 of
+        // them, fill_desc), 8 when all are small
+        bool any_large = false;
+        for (uint32_t i = 0; i < n; ++i)
+            any_large |= uint64_t(ceil_div(Ls[i].tiles, G)) * Ls[i].ns > kSmallLayerUnits;
+        sp.consumers = any_large && per_layer_nca_enabled() ? kStackConsumersDefault : 8u;
+        if (!per_layer_nca_enabled()) {  // the round-1 rule: mean units per layer
+            uint64_t units = 0;
+            for (uint32_t i = 0; i < n; ++i) units += uint64_t(ceil_div(Ls[i].tiles, G)) * Ls[i].ns;
+            sp.consumers = units <= kSmallLayerUnits * n ? 8u : kStackConsumersDefault;
+        }
     }
     if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
         const int c = atoi(e);
@@ -317,7 +343,7 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.k31 = 1u << 31;
     sp.kneg = 0xffffffffu;
     for (uint32_t i = 0; i < n && i < kInlineLayers; ++i)
-        fill_desc(sp.inl[i], Ls[i], sp.slot_bytes, bits, G);
+        fill_desc(sp.inl[i], Ls[i], sp.slot_bytes, bits, G, sp.consumers);
     return DSQ_OK;
 }
 
@@ -1409,7 +1435,7 @@ static int stack_create_impl(dsq_cuda_layer* const* layers, uint32_t n, const in
     uint32_t ord = 0;
     for (uint32_t i = 0; i < n; ++i) {
         StackLayerDesc& d = descs[i];
-        fill_desc(d, pl[i], S->sp.slot_bytes, L0->bits, G);
+        fill_desc(d, pl[i], S->sp.slot_bytes, L0->bits, G, S->sp.consumers);
         const dsq_cuda_layer* L = layers[i];
         d.idx = L->rec;
         d.lut = L->tlut;

@@ -69,7 +69,7 @@ __device__ __forceinline__ const StackLayerDesc& layer_desc(const StackParams& p
 
 // CTA tile share from the host-precomputed quotient/remainder (no division)
 struct Share {
-    uint32_t t0, nt, nch;  // first tile, tiles, ring chunks
+    uint32_t t0, nt;       // first tile, tiles
     uint32_t r0, nrows;    // real rows [r0, r0 + nrows) (tiles clipped to the layer)
 };
 __device__ __forceinline__ Share cta_share(const StackLayerDesc& d, uint32_t cta) {
@@ -77,7 +77,6 @@ __device__ __forceinline__ Share cta_share(const StackLayerDesc& d, uint32_t cta
     const bool hi = cta < d.tr;
     s.t0 = cta * d.tq + (hi ? cta : d.tr);
     s.nt = d.tq + (hi ? 1u : 0u);
-    s.nch = hi ? d.nch_hi : d.nch_lo;
     s.r0 = min(s.t0 * kTileRows, d.rows);
     s.nrows = min((s.t0 + s.nt) * kTileRows, d.rows) - s.r0;
     return s;
@@ -712,8 +711,10 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 if (pl >= p.n_layers) return;
                 const SDesc& sn = desc_wait(pl);
                 const uint32_t Un = sn.nt * sn.d.ns;
-                pa = (cw * Un) / NC;
-                pe = ((cw + 1) * Un) / NC;
+                // warps past the layer's active count own no units of it
+                const bool act = cw < sn.d.nca;
+                pa = act ? (cw * Un) >> sn.d.nca_shift : 0u;
+                pe = act ? ((cw + 1) * Un) >> sn.d.nca_shift : 0u;
                 pcu = sn.d.cu;
                 psrc = sn.d.idx + (size_t(sn.t0) * sn.d.ns + pa) * UW;
                 pvalid = true;
@@ -779,7 +780,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         // follow the warp across chunks and are flushed into part[cw][row]
         // on a tile change.
         const uint32_t U = sd.nt * NS;
-        const uint32_t u0 = (cw * U) / NC, u1 = ((cw + 1) * U) / NC;
+        const bool act = cw < d.nca;
+        const uint32_t u0 = act ? (cw * U) >> d.nca_shift : 0u;
+        const uint32_t u1 = act ? ((cw + 1) * U) >> d.nca_shift : 0u;
         uint32_t cur_tile = 0xffffffffu;
         Planes16 P;
         float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};

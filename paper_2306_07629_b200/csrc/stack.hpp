@@ -73,8 +73,10 @@ struct StackLayerDesc {
                                 // (row-parallel) layers, kNoDep if its y is final
     // host-precomputed tile split over the grid (no device division):
     // CTA c owns tiles [c*tq + min(c, tr), ...) -- tq or tq+1 tiles -- whose
-    // units are streamed in chunks of cu units (nch_lo / nch_hi chunks)
-    uint32_t tq, tr, cu, nch_lo, nch_hi;
+    // units are streamed in chunks of cu units by the layer's first
+    // nca = 1 << nca_shift consumer warps (the rest skip the layer: a layer
+    // that gives a CTA few units runs on 8 of 16 warps, twice the units each)
+    uint32_t tq, tr, cu, nca, nca_shift;
 };
 
 struct StackParams {

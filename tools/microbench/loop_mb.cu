@@ -659,6 +659,112 @@ __global__ void __launch_bounds__(1024, 1) k_flat(const uint32_t* __restrict__ g
     out[blockIdx.x * blockDim.x + threadIdx.x] = part[lane] + d0[0] + d1[1];
 }
 
+// V11: k_flat with cross-layer software pipelining: the next layer's LUT
+// planes and the current pair's words/x are always loaded one pair ahead
+// (the pair loop carries the loaded operands in registers across the tile
+// change and the layer boundary), so a restart never exposes the LDS latency
+__global__ void __launch_bounds__(1024, 1) k_pipe(const uint32_t* __restrict__ g, int L, int U,
+                                                  int NS, int consumers, float* out, ShiftK K,
+                                                  long long* clk, int mode = 0) {
+    extern __shared__ __align__(1024) uint8_t smb[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smb);
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smb + 2048);
+    float* part = reinterpret_cast<float*>(smb + 2048 + 64 * 256 * 2);
+    uint32_t* luts = reinterpret_cast<uint32_t*>(smb + 2048 + 64 * 512 + 16 * 1024);
+    uint8_t* ring = smb + 2048 + 64 * 512 + 16 * 1024 + 4096;
+    const uint32_t slot_bytes = ((U * 384 + 127) / 128) * 128;
+    for (uint32_t i = threadIdx.x; i < 64 * 256; i += blockDim.x) xs[i] = uint16_t(0x3800 + (i & 0x3ff));
+    for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) luts[i] = 0x3c3a3836u ^ i;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < consumers * 2; ++i) mbar_init(&full[i], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (int(warp) >= consumers) return;
+    const uint64_t pol = policy_evict_first();
+    const size_t wbase = (size_t(blockIdx.x) * consumers + warp) * size_t(L) * U * 96;
+    auto issue = [&](int l) {
+        if (l >= L || ((mode & 4) && l >= 2)) return;
+        if (lane == 0) {
+            uint64_t* bar = &full[warp * 2 + (l & 1)];
+            mbar_arrive_expect_tx(bar, U * 384);
+            bulk_g2s(ring + size_t(warp * 2 + (l & 1)) * slot_bytes, g + wbase + size_t(l) * U * 96,
+                     U * 384, bar, pol);
+        }
+    };
+    issue(0);
+    issue(1);
+    const ShiftK k = K;
+    const uint32_t xoff = tile_x_offset(lane), trow = (lane >> 2) & 3u;
+    const uint32_t s_start = (warp * U) % NS, t_start = (warp * U) / NS;
+    long long c0 = clock64();
+    float d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
+    // unit cursor state (units of the warp's whole stream: L layers x U)
+    int l = 0, u = 0;
+    uint32_t s = s_start, tile = t_start;
+    const uint32_t* sp = nullptr;
+    const uint16_t* xh = nullptr;
+    auto enter_layer = [&](int ll) {
+        if (!(mode & 4) || ll < 2) mbar_wait(&full[warp * 2 + (ll & 1)], (ll >> 1) & 1u);
+        sp = reinterpret_cast<const uint32_t*>(ring + size_t(warp * 2 + (ll & 1)) * slot_bytes) + lane;
+        xh = xs + (ll & 3) * 4096 + xoff;
+        s = s_start;
+        tile = t_start;
+    };
+    enter_layer(0);
+    uint4 q0 = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
+    Planes8 P{q0.x, q0.y, q0.z, q0.w};
+    // operands of the next unit, loaded ahead
+    uint32_t w0 = sp[0], w1 = sp[32], w2 = sp[64];
+    uint4 xa = ldx(xh + (s & 15) * 256, 0), xb = ldx(xh + (s & 15) * 256, 128);
+    int parity = 0;
+    const int total = L * U;
+    for (int n = 0; n < total; ++n) {
+        const uint32_t cw0 = w0, cw1 = w1, cw2 = w2;
+        const uint4 cxa = xa, cxb = xb;
+        const Planes8 CP = P;
+        // advance the cursor to the next unit and load its operands now
+        ++u;
+        ++s;
+        sp += 96;
+        bool flush_after = false;
+        if (u == U) {  // layer end: flush after this unit, next layer
+            flush_after = true;
+            __syncwarp();
+            issue(l + 1 + 1 - 1 + 1);  // refill the slot of layer l with layer l + 2
+            ++l;
+            u = 0;
+            if (l < L) enter_layer(l);
+        } else if (s == uint32_t(NS)) {  // tile end
+            flush_after = true;
+            s = 0;
+            ++tile;
+        }
+        if (n + 1 < total) {
+            w0 = sp[0]; w1 = sp[32]; w2 = sp[64];
+            xa = ldx(xh + (s & 15) * 256, 0);
+            xb = ldx(xh + (s & 15) * 256, 128);
+            if (flush_after) {
+                const uint4 q = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
+                P = Planes8{q.x, q.y, q.z, q.w};
+            }
+        }
+        if (parity == 0) span3_mma_one(cw0, cw1, cw2, CP, cxa, cxb, d0, k);
+        else span3_mma_one(cw0, cw1, cw2, CP, cxa, cxb, d1, k);
+        parity ^= 1;
+        if (flush_after && !(mode & 2)) {
+            const float v = tile_rows_reduce(d0, d1, lane);
+            if ((lane & 3) == 0 && lane < 16) part[warp * 256 + ((tile * 4 + trow) & 255)] += v;
+#pragma unroll
+            for (int z = 0; z < 4; ++z) d0[z] = d1[z] = 0.f;
+        }
+    }
+    long long c1 = clock64();
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(clk), c1 - c0);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = part[lane] + d0[0] + d1[1];
+}
+
 int main(int argc, char** argv) {
     cudaDeviceProp pr;
     CK(cudaGetDeviceProperties(&pr, 0));
@@ -736,19 +842,22 @@ int main(int argc, char** argv) {
             ldg(k_ldg<4>, "V7 ldg D=4 pairs", c);
             ldg(k_ldg<6>, "V7 ldg D=6 pairs", c);
         }
-        auto lay = [&](int c, int U, int NS, bool use_ldg = false, int mode = 0, bool flat = false) -> int {
+        auto lay = [&](int c, int U, int NS, bool use_ldg = false, int mode = 0, int flat = 0) -> int {
             const int L = int(total_units / nsm / c / U);
             const size_t smem = 2048 + 64 * 512 + 16 * 1024 + 4096 + size_t(c) * 2 * (((U * 384 + 127) / 128) * 128);
             if (smem > 227 * 1024) return 0;
             CK(cudaFuncSetAttribute(k_flat, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            CK(cudaFuncSetAttribute(k_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             if (use_ldg) CK(cudaFuncSetAttribute(k_layers_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             else CK(cudaFuncSetAttribute(k_layers, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
+            if (flat == 2) k_pipe<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
+            else if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
             else if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk);
             else k_layers<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
             CK(cudaDeviceSynchronize());
             cudaEventRecord(e0);
-            if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
+            if (flat == 2) k_pipe<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
+            else if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
             else if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk);
             else k_layers<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
             cudaEventRecord(e1);
@@ -756,16 +865,16 @@ int main(int argc, char** argv) {
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
             const double w = double(nsm) * c * L * U * 1024.0;
-            printf("%s mode %d ", flat ? "FLAT" : "seg ", mode);
+            printf("%s mode %d ", flat == 2 ? "PIPE" : flat ? "FLAT" : "seg ", mode);
             printf(use_ldg ? "V9 ldg    c%2d U %3d NS %2d: %.3f ms  %6.1f w/clk/SM @1.965  %6.0f GB/s  %.0f ns/layer\n" : "V8 layers c%2d U %3d NS %2d: %.3f ms  %6.1f w/clk/SM @1.965  %6.0f GB/s  %.0f ns/layer\n", c, U, NS,
                    ms, w / (ms * 1e-3) / nsm / 1.965e9, w * 0.375 / (ms * 1e-3) / 1e9, ms * 1e6 / L);
             return 0;
         };
         if (argc > 1) {  // one configuration: c U NS mode flat
-            lay(atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), false, atoi(argv[4]), atoi(argv[5]) != 0);
+            lay(atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), false, atoi(argv[4]), atoi(argv[5]));
             return 0;
         }
-        for (int flat = 0; flat < 2; ++flat) {
+        for (int flat = 0; flat < 3; flat += 2) {
             for (int mode : {0, 4, 6}) lay(8, 14, 16, false, mode, flat);
             for (int mode : {0, 6}) lay(8, 28, 16, false, mode, flat);
             for (int mode : {0, 6}) lay(8, 37, 16, false, mode, flat);
