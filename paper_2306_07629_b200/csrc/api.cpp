@@ -43,8 +43,11 @@ cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut
                          float* part, uint32_t kslices, uint32_t spans_per_slice, int mode,
                          cudaStream_t st);
 cudaError_t launch_apply_deltas(const uint32_t* row_ptr, const uint32_t* csr, const uint16_t* lut,
-                                uint32_t K, uint32_t rows, uint32_t cols, float* w,
-                                cudaStream_t st);
+                                uint32_t K, uint32_t groups, uint32_t gcols, uint32_t rows,
+                                uint32_t cols, float* w, cudaStream_t st);
+cudaError_t launch_grouped(int mode, const GroupedParams& p, const uint16_t* x, void* y, bool y_f16,
+                           cudaStream_t st, bool pdl);
+cudaError_t launch_grouped_decode(int mode, const GroupedParams& p, void* out, cudaStream_t st);
 cudaError_t launch_dense_f32(const float* w, uint32_t rows, uint32_t cols, const float* x,
                              double* y, int num_sms, cudaStream_t st);
 cudaError_t launch_dump_frags(uint32_t bits, const uint32_t* idx, const uint32_t* lut,
@@ -377,6 +380,8 @@ struct dsq_cuda_layer {
     uint16_t* dense_w = nullptr;  // lazily materialized fp16 dense W (reference kernel)
     // tile-record layout (bits 3/4): the persistent stack kernel's format
     bool rec_layout = false;
+    bool grouped = false;                   // groups_per_row > 1: reference layout, grouped_gemv
+    GroupedParams G{};
     uint32_t tiles = 0, ns = 0;
     const uint32_t* tlut = nullptr;         // LUT planes [tiles][4][LW]
     const uint32_t* rec = nullptr;
@@ -478,13 +483,93 @@ static int validate_view(const dsq_layer_view* v) {
         return fail(DSQ_E_SHAPE_MISMATCH, "%s: packed dims mismatch", v->name);
     if (s.rows != v->rows || s.cols != v->cols)
         return fail(DSQ_E_SHAPE_MISMATCH, "%s: sparse dims mismatch", v->name);
-    if (p.groups_per_row != 1)
-        return fail(DSQ_E_UNSUPPORTED,
-                    "%s: device path implements channel-wise LUTs (groups_per_row == 1)", v->name);
     return DSQ_OK;
 }
 
 int dsq_internal_validate_view(const dsq_layer_view* v) { return validate_view(v); }
+
+// Grouped-LUT layers (groups_per_row > 1, the grouping ablation): the
+// reference payload uploaded as is, fp16 LUTs [rows][groups][K], the CSR as
+// the other layouts; products by grouped_gemv (kernels.cu), no stack support.
+static int create_grouped(const dsq_layer_view* v, int device, int num_sms, dsq_cuda_layer** out) {
+    auto* L = new dsq_cuda_layer;
+    L->device = device;
+    L->num_sms = num_sms;
+    L->name = v->name;
+    L->rows = v->rows;
+    L->cols = v->cols;
+    L->bits = v->packed.bits;
+    L->groups = v->packed.groups_per_row;
+    L->nnz = v->sparse.nnz;
+    L->hybrid_top_k = v->hybrid_top_k;
+    L->grouped = true;
+    const uint32_t rows = L->rows, cols = L->cols, bits = L->bits, groups = L->groups;
+    const uint32_t K = 1u << bits;
+    L->algorithmic_bytes = dsq_bytes_touched_estimate(rows, cols, bits, cols / groups, L->nnz);
+    const size_t nl = size_t(rows) * groups * K;
+    std::vector<uint16_t> lut(nl);
+    for (size_t i = 0; i < nl; ++i) {
+        if (v->packed.luts_f16) {
+            lut[i] = v->packed.luts_f16[i];
+        } else {
+            const float f = v->packed.luts_f32[i];
+            lut[i] = f32_to_f16(f);
+            if (f16_to_f32(lut[i]) != f) L->luts_exact = 0;
+        }
+        if ((lut[i] & 0x7c00u) == 0x7c00u) {
+            delete L;
+            return fail(DSQ_E_NON_FINITE_VALUE, "%s: LUT centroid %zu is not finite in fp16",
+                        v->name, i);
+        }
+    }
+    std::vector<uint32_t> csr(std::max<uint32_t>(L->nnz, 1), 0);
+    for (uint32_t q = 0; q < L->nnz; ++q) {
+        uint16_t h;
+        if (v->sparse.values_f16) {
+            h = v->sparse.values_f16[q];
+        } else {
+            h = f32_to_f16(v->sparse.values_f32[q]);
+            if (f16_to_f32(h) != v->sparse.values_f32[q]) L->values_exact = 0;
+        }
+        csr[q] = uint32_t(v->sparse.col_idx[q]) | (uint32_t(h) << 16);
+    }
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t pay = v->packed.payload_len;
+    const size_t o_pay = 0, o_lut = al(pay + 16), o_rp = o_lut + al(nl * 2),
+                 o_csr = o_rp + al((size_t(rows) + 1) * 4), o_x16 = o_csr + al(csr.size() * 4),
+                 total = o_x16 + al((size_t(cols) + 8) * 2);
+    cudaError_t e = cudaMalloc(&L->arena, total);
+    if (e != cudaSuccess) {
+        delete L;
+        return cuda_fail(e, "cudaMalloc(grouped layer)");
+    }
+    L->arena_bytes = total;
+    uint8_t* base = static_cast<uint8_t*>(L->arena);
+    if ((e = cudaMemcpy(base + o_pay, v->packed.payload, pay, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(base + o_lut, lut.data(), nl * 2, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(base + o_rp, v->sparse.row_ptr, (size_t(rows) + 1) * 4,
+                        cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(base + o_csr, csr.data(), csr.size() * 4, cudaMemcpyHostToDevice)) !=
+            cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        dsq_cuda_layer_destroy(L);
+        return cuda_fail(e, "grouped layer upload");
+    }
+    L->G = GroupedParams{base + o_pay, reinterpret_cast<const uint16_t*>(base + o_lut),
+                         reinterpret_cast<const uint32_t*>(base + o_rp),
+                         reinterpret_cast<const uint32_t*>(base + o_csr), rows, cols, bits, groups,
+                         cols / groups, uint32_t(row_stride(cols, bits))};
+    L->P.row_ptr = L->G.row_ptr;
+    L->P.csr = L->G.csr;
+    L->P.lut = L->G.lut;
+    L->P.rows = rows;
+    L->P.cols = cols;
+    L->P.bits = bits;
+    L->P.nnz = L->nnz;
+    L->x16 = reinterpret_cast<uint16_t*>(base + o_x16);
+    *out = L;
+    return DSQ_OK;
+}
 
 int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** out) {
     if (!out) return fail(DSQ_E_INVALID_ARGUMENT, "null output handle");
@@ -499,6 +584,7 @@ int dsq_cuda_layer_create(const dsq_layer_view* v, int device, dsq_cuda_layer** 
     int num_sms = 0;
     if ((rc = query_num_sms(device, &num_sms))) return rc;
 
+    if (v->packed.groups_per_row > 1) return create_grouped(v, device, num_sms, out);
     auto* L = new dsq_cuda_layer;
     L->device = device;
     L->num_sms = num_sms;
@@ -812,7 +898,7 @@ int dsq_cuda_layer_get_info(const dsq_cuda_layer* L, dsq_layer_info* info) {
     info->rows = L->rows;
     info->cols = L->cols;
     info->bits = L->bits;
-    info->groups_per_row = 1;
+    info->groups_per_row = L->groups;
     info->nnz = L->nnz;
     info->device_bytes = L->arena_bytes + (L->dense_w ? size_t(L->rows) * L->cols * 2 : 0);
     info->algorithmic_bytes = L->algorithmic_bytes;
@@ -827,7 +913,9 @@ static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(L->mu);
     if (L->dense_w) return DSQ_OK;
     CUDA_TRY(cudaMalloc(&L->dense_w, size_t(L->rows) * L->cols * 2));
-    if (L->rec_layout)
+    if (L->grouped)
+        CUDA_TRY(launch_grouped_decode(1, L->G, L->dense_w, st));
+    else if (L->rec_layout)
         CUDA_TRY(launch_decode_tiles(1, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns,
                                      L->dense_w, st));
     else
@@ -881,6 +969,33 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
     if (!x_stride) x_stride = L->cols;
     if (!y_stride) y_stride = L->rows;
     if (batch < 1 || batch > 16) return fail(DSQ_E_INVALID_ARGUMENT, "batch must be 1..16");
+    if (L->grouped && kernel != DSQ_KERNEL_REFERENCE) {
+        // grouped LUTs: one grouped_gemv launch per vector
+        if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_FUSED)
+            return fail(DSQ_E_INVALID_ARGUMENT, "unknown kernel %d", kernel);
+        if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
+            return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
+        if (x_dtype == DSQ_F32 && batch != 1)
+            return fail(DSQ_E_INVALID_ARGUMENT, "batched x must be F16");
+        const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
+        const size_t ysz = y_dtype == DSQ_F16 ? 2 : 4;
+        for (uint32_t b = 0; b < batch; ++b) {
+            const uint16_t* xb;
+            if (x_dtype == DSQ_F32) {
+                CUDA_TRY(launch_f32_to_f16(static_cast<const float*>(x), L->x16, L->cols, st, pdl));
+                xb = L->x16;
+            } else if (x_dtype == DSQ_F16) {
+                xb = static_cast<const uint16_t*>(x) + size_t(b) * x_stride;
+            } else {
+                return fail(DSQ_E_INVALID_ARGUMENT, "x dtype must be F32 or F16");
+            }
+            CUDA_TRY(launch_grouped(mode, L->G, xb, static_cast<uint8_t*>(y) + size_t(b) * y_stride * ysz,
+                                    y_dtype == DSQ_F16, st, pdl));
+        }
+        return DSQ_OK;
+    }
+    if (L->grouped && batch > 1)
+        return fail(DSQ_E_UNSUPPORTED, "grouped LUTs: batched reference kernel");
     const uint32_t nbk = batch == 2 ? 2u : batch <= 4 ? 4u : 8u;
     if (batch >= 2 && batch <= 8 && L->rec_layout && !L->k7_batch_failed(nbk) &&
         (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
@@ -1131,7 +1246,9 @@ int dsq_cuda_matvec_host(const dsq_cuda_layer* Lc, int kernel, const float* x_ho
 int dsq_cuda_unpack(const dsq_cuda_layer* L, uint16_t* assign_dev, void* stream) {
     if (!L || !assign_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     cudaSetDevice(L->device);
-    if (L->rec_layout)
+    if (L->grouped)
+        CUDA_TRY(launch_grouped_decode(0, L->G, assign_dev, static_cast<cudaStream_t>(stream)));
+    else if (L->rec_layout)
         CUDA_TRY(launch_decode_tiles(0, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns,
                                      assign_dev, static_cast<cudaStream_t>(stream)));
     else
@@ -1145,7 +1262,9 @@ int dsq_cuda_dequant(const dsq_cuda_layer* L, void* w_dev, int out_dtype, void* 
         return fail(DSQ_E_INVALID_ARGUMENT, "dequant: out dtype must be F16 or F32");
     cudaSetDevice(L->device);
     const int mode = out_dtype == DSQ_F16 ? 1 : 2;
-    if (L->rec_layout)
+    if (L->grouped)
+        CUDA_TRY(launch_grouped_decode(mode, L->G, w_dev, static_cast<cudaStream_t>(stream)));
+    else if (L->rec_layout)
         CUDA_TRY(launch_decode_tiles(mode, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns,
                                      w_dev, static_cast<cudaStream_t>(stream)));
     else
@@ -1169,14 +1288,16 @@ int dsq_cuda_dequantize_layer(const dsq_cuda_layer* L, float* w_dev, void* strea
     if (!L || !w_dev) return fail(DSQ_E_INVALID_ARGUMENT, "null argument");
     cudaSetDevice(L->device);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (L->rec_layout)
+    if (L->grouped)
+        CUDA_TRY(launch_grouped_decode(2, L->G, w_dev, st));
+    else if (L->rec_layout)
         CUDA_TRY(launch_decode_tiles(2, L->bits, L->rec, L->tlut, L->rows, L->cols, L->ns, w_dev,
                                      st));
     else
         CUDA_TRY(launch_decode(2, L->P, w_dev, st));
     if (L->nnz)
-        CUDA_TRY(launch_apply_deltas(L->P.row_ptr, L->P.csr, L->P.lut, 1u << L->bits, L->rows,
-                                     L->cols, w_dev, st));
+        CUDA_TRY(launch_apply_deltas(L->P.row_ptr, L->P.csr, L->P.lut, 1u << L->bits, L->groups,
+                                     L->cols / L->groups, L->rows, L->cols, w_dev, st));
     return DSQ_OK;
 }
 

@@ -470,28 +470,112 @@ cudaError_t launch_dense(const uint16_t* w, uint32_t rows, uint32_t cols, const 
                               static_cast<float*>(y));
 }
 
+// ---------------------------------------------------------------------------
+// Grouped LUTs (groups_per_row > 1, the reference's grouping ablation,
+// packfmt.hpp:28-31): the reference packed layout read directly (LSB-first
+// bitstream rows, packfmt.cpp:40-53) and lut_at(r, c) = luts[(r * groups +
+// c / gcols) * K], as in lut_row_dot (kernels.cpp:18-33).  One warp per row,
+// exact fp16 x fp16 products accumulated in fp32.  MODE 0 LUT, 1 CSR, 2 fused.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t grouped_index(const uint8_t* row, uint32_t stride, uint32_t c,
+                                                  uint32_t bits) {
+    const uint32_t bp = c * bits, b = bp >> 3;
+    const uint32_t w = uint32_t(row[b]) | (b + 1 < stride ? uint32_t(row[b + 1]) << 8 : 0u);
+    return (w >> (bp & 7u)) & ((1u << bits) - 1u);
+}
+
+template <typename YT, int MODE>
+__global__ void grouped_gemv(const GroupedParams p, const uint16_t* __restrict__ x,
+                             YT* __restrict__ y) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    pdl_wait();
+    pdl_trigger();
+    if (r >= p.rows) return;
+    const uint32_t K = 1u << p.bits;
+    float acc = 0.f;
+    if (MODE != 1) {
+        const uint8_t* row = p.payload + size_t(r) * p.stride;
+        const uint16_t* lr = p.lut + size_t(r) * p.groups * K;
+        for (uint32_t c = lane; c < p.cols; c += 32) {
+            const uint32_t idx = grouped_index(row, p.stride, c, p.bits);
+            acc = fma_h(lr[(c / p.gcols) * K + idx], x[c], acc);
+        }
+    }
+    if (MODE != 0) {
+        for (uint32_t q = p.row_ptr[r] + lane; q < p.row_ptr[r + 1]; q += 32) {
+            const uint32_t e = p.csr[q];
+            acc = fma_h(uint16_t(e >> 16), x[e & 0xffffu], acc);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) store_y<YT>(y, r, acc);
+}
+
+// K5 / K6 for grouped layers: MODE 0 u16 indices, 1 fp16 values, 2 fp32 values
+template <int MODE>
+__global__ void grouped_decode(const GroupedParams p, void* out) {
+    const size_t t = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= size_t(p.rows) * p.cols) return;
+    const uint32_t r = uint32_t(t / p.cols), c = uint32_t(t % p.cols);
+    const uint32_t idx = grouped_index(p.payload + size_t(r) * p.stride, p.stride, c, p.bits);
+    const uint16_t h = p.lut[(size_t(r) * p.groups + c / p.gcols) * (1u << p.bits) + idx];
+    if (MODE == 0) static_cast<uint16_t*>(out)[t] = uint16_t(idx);
+    else if (MODE == 1) static_cast<uint16_t*>(out)[t] = h;
+    else static_cast<float*>(out)[t] = __half2float(__ushort_as_half(h));
+}
+
+cudaError_t launch_grouped(int mode, const GroupedParams& p, const uint16_t* x, void* y, bool y_f16,
+                           cudaStream_t st, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((p.rows + 7) / 8);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define DSQ_G(T, M) cudaLaunchKernelEx(&cfg, grouped_gemv<T, M>, p, x, static_cast<T*>(y))
+    if (y_f16) return mode == 0 ? DSQ_G(__half, 0) : mode == 1 ? DSQ_G(__half, 1) : DSQ_G(__half, 2);
+    return mode == 0 ? DSQ_G(float, 0) : mode == 1 ? DSQ_G(float, 1) : DSQ_G(float, 2);
+#undef DSQ_G
+}
+
+cudaError_t launch_grouped_decode(int mode, const GroupedParams& p, void* out, cudaStream_t st) {
+    const size_t n = size_t(p.rows) * p.cols;
+    const uint32_t blocks = uint32_t((n + 255) / 256);
+    if (mode == 0) grouped_decode<0><<<blocks, 256, 0, st>>>(p, out);
+    else if (mode == 1) grouped_decode<1><<<blocks, 256, 0, st>>>(p, out);
+    else grouped_decode<2><<<blocks, 256, 0, st>>>(p, out);
+    return cudaGetLastError();
+}
+
 // dequantize_layer (pipeline.cpp:49-75), second half: after the LUT dequant
 // (K6, fp32) every extracted position becomes lut_row[0] + delta, one fp32
 // addition like the reference's float arithmetic (the widened fp16 operands
 // are exact).  One warp per row, entries in CSR order.
 __global__ void apply_deltas(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
-                             const uint16_t* __restrict__ lut, uint32_t K, uint32_t rows,
-                             uint32_t cols, float* __restrict__ w) {
+                             const uint16_t* __restrict__ lut, uint32_t K, uint32_t groups,
+                             uint32_t gcols, uint32_t rows, uint32_t cols, float* __restrict__ w) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= rows) return;
-    const float l0 = __half2float(__ushort_as_half(lut[size_t(r) * K]));
     for (uint32_t q = row_ptr[r] + lane; q < row_ptr[r + 1]; q += 32) {
-        const uint32_t e = csr[q];
+        const uint32_t e = csr[q], c = e & 0xffffu;
+        // lut_at(r, c)[0]: the codebook of c's group (packfmt.hpp:28-31)
+        const float l0 = __half2float(__ushort_as_half(lut[(size_t(r) * groups + c / gcols) * K]));
         const float d = __half2float(__ushort_as_half(uint16_t(e >> 16)));
-        w[size_t(r) * cols + (e & 0xffffu)] = __fadd_rn(l0, d);
+        w[size_t(r) * cols + c] = __fadd_rn(l0, d);
     }
 }
 
 cudaError_t launch_apply_deltas(const uint32_t* row_ptr, const uint32_t* csr, const uint16_t* lut,
-                                uint32_t K, uint32_t rows, uint32_t cols, float* w,
-                                cudaStream_t st) {
-    apply_deltas<<<(rows + 7) / 8, 256, 0, st>>>(row_ptr, csr, lut, K, rows, cols, w);
+                                uint32_t K, uint32_t groups, uint32_t gcols, uint32_t rows,
+                                uint32_t cols, float* w, cudaStream_t st) {
+    apply_deltas<<<(rows + 7) / 8, 256, 0, st>>>(row_ptr, csr, lut, K, groups, gcols, rows, cols,
+                                                 w);
     return cudaGetLastError();
 }
 

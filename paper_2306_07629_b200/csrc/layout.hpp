@@ -55,6 +55,16 @@ struct LayerParams {
     uint32_t rows, cols, bits, n_rb, ng, n_workers, nnz;
 };
 
+// A grouped-LUT layer (groups_per_row > 1, kernels.cu grouped_gemv): the
+// reference packed layout as is, LUTs per (row, column group).
+struct GroupedParams {
+    const uint8_t* payload;   // rows x stride bytes (reference layout)
+    const uint16_t* lut;      // fp16 [rows][groups][K]
+    const uint32_t* row_ptr;  // CSR row pointers [rows+1]
+    const uint32_t* csr;      // col | fp16(delta) << 16
+    uint32_t rows, cols, bits, groups, gcols, stride;
+};
+
 // The balanced schedule travels as a __grid_constant__ kernel parameter
 // (constant bank, pushed with the launch): no dependent global load is needed
 // before a warp knows its range.  Worker w owns units [u0[w], u0[w+1]).

@@ -59,3 +59,44 @@ def test_bare_packed_and_csr_products(torch, oracle):
     assert np.abs(lut_matvec(q.packed, x) - ref).max() <= 1e-5 * np.abs(ref).max()
     ref = oracle.csr_matvec(L, x)
     assert np.abs(csr_matvec(q.sparse, x) - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("rows,cols,bits,groups,sp", [(64, 256, 3, 4, 0.0045), (33, 96, 4, 2, 0.02),
+                                                      (40, 128, 2, 8, 0.01), (17, 120, 5, 3, 0.05),
+                                                      (512, 4096, 3, 32, 0.0045)])
+def test_grouped_luts_on_device(torch, oracle, reference, rows, cols, bits, groups, sp):
+    """Grouped LUTs (groups_per_row > 1, the grouping ablation,
+    packfmt.hpp:28-31 / kernels.cpp:21-30) through the device products:
+    unpack / dequant bit-exact, products within the fp32-accumulation
+    tolerance, dequantize_layer bit-exact against the reference."""
+    import ctypes as C
+    import paper_2306_07629_b200._native as N
+    from paper_2306_07629_b200 import DeviceLayer, dequantize_layer, fused_dns_matvec, lut_matvec
+    L = make_layer(rows, cols, bits, sp, seed=rows + groups * 7 + bits, skew="zipf", groups=groups)
+    q = to_quantized_layer(L)
+    dl = DeviceLayer(q)
+    assert dl.info().groups_per_row == groups
+    a = torch.empty(rows * cols, dtype=torch.int16, device="cuda")
+    dl.unpack(a.data_ptr())
+    w = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
+    dl.dequant(w.data_ptr(), 0)
+    torch.cuda.synchronize()
+    rc, assign = oracle.unpack(L.payload, bits, rows, cols)
+    assert rc == 0 and np.array_equal(a.cpu().numpy().view(np.uint16), assign)
+    assert np.array_equal(w.cpu().numpy(), oracle.dequant_dense(L))
+    x = make_x(cols, seed=5).astype(np.float32)
+    ref = oracle.fused_dns_matvec(L, x, 10)
+    y = fused_dns_matvec(q, x)
+    assert np.abs(y - ref).max() <= 1e-5 * max(np.abs(ref).max(), 1e-30)
+    refl = oracle.lut_matvec(L, x)
+    assert np.abs(lut_matvec(q.packed, x) - refl).max() <= 1e-5 * max(np.abs(refl).max(), 1e-30)
+    # device products on device buffers, fp16 x / fp32 y
+    xt = torch.from_numpy(x.astype(np.float16).view(np.int16)).cuda()
+    yt = torch.empty(rows, dtype=torch.float32, device="cuda")
+    dl.gemv(N.KERNEL_FUSED, xt.data_ptr(), N.F16, yt.data_ptr(), N.F32)
+    torch.cuda.synchronize()
+    assert np.abs(yt.cpu().numpy() - ref).max() <= 1e-5 * max(np.abs(ref).max(), 1e-30)
+    want = np.zeros(rows * cols, np.float32)
+    rl = reference.layer(L)
+    assert reference.lib.ref_dequantize_layer(rl.h, C.c_void_p(want.ctypes.data)) == 0
+    assert np.array_equal(dequantize_layer(q).reshape(-1).view(np.uint32), want.view(np.uint32))

@@ -105,11 +105,18 @@ def test_validation_dims(good):
     assert _errc(good) == 9
 
 
-def test_grouped_luts_unsupported_on_device():
-    L = to_quantized_layer(make_layer(4, 64, 3, 0.0, seed=2))
-    L.packed.groups_per_row = 2
-    L.packed.luts = np.concatenate([L.packed.luts, L.packed.luts])
-    assert _errc(L) == 102
+def test_grouped_luts_pass_validation():
+    """groups_per_row > 1 (the grouping ablation) is a valid device layer now
+    (grouped_gemv); on a host without a GPU the upload then fails with
+    no_device, never with unsupported / shape_mismatch."""
+    from conftest import has_gpu
+    from paper_2306_07629_b200 import DeviceLayer
+    L = to_quantized_layer(make_layer(4, 64, 3, 0.0, seed=2, groups=2))
+    assert L.packed.groups_per_row == 2
+    if has_gpu():
+        assert DeviceLayer(L).info().groups_per_row == 2
+    else:
+        assert _errc(L) == 101
 
 
 def test_no_gpu_fails_loudly(good):

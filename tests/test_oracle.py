@@ -181,3 +181,19 @@ def test_restatement_matches_reference_live(oracle, reference, rows, cols, bits,
     assert np.array_equal(rl.matvec("csr", x), oracle.csr_matvec(L, x))
     assert np.array_equal(rl.matvec("fused", x), oracle.fused_dns_matvec(L, x, 10, nthreads=4))
     assert np.array_equal(rl.dequant_dense(), oracle.dequant_dense(L))
+
+
+@pytest.mark.parametrize("rows,cols,bits,groups", [(16, 128, 3, 4), (9, 96, 4, 2), (5, 64, 2, 8),
+                                                   (7, 120, 5, 3)])
+def test_grouped_restatement_matches_reference(oracle, reference, rows, cols, bits, groups):
+    """Grouped LUTs (lut_at(r, c) = luts[(r*groups + c/gcols)*K], packfmt.hpp:28-31):
+    the restated products and dequant equal the compiled reference bit for bit."""
+    import ctypes as C
+    L = make_layer(rows, cols, bits, 0.02, seed=rows * groups + bits, groups=groups)
+    x = make_x(cols, seed=3).astype(np.float32)
+    rl = reference.layer(L)
+    assert np.array_equal(rl.matvec("lut", x), oracle.lut_matvec(L, x))
+    assert np.array_equal(rl.matvec("fused", x), oracle.fused_dns_matvec(L, x, 10))
+    assert np.array_equal(rl.dequant_dense(), oracle.dequant_dense(L))
+    want = np.zeros(rows * cols, np.float32)
+    assert reference.lib.ref_dequantize_layer(rl.h, C.c_void_p(want.ctypes.data)) == 0
