@@ -103,6 +103,36 @@ __global__ void __launch_bounds__(1024, 1) k_loop(int niter, float* out, int con
                 span3_mma_one(c0_, c1, c2, PA, xa2, xb2, d2, k);
                 span3_mma_one(e0, e1, e2, PA, xa3, xb3, d3, k);
             }
+        } else if constexpr (VAR == 7 || VAR == 8) {
+            // V0 split into "layers" of 14 units (7 pairs): a loop restart per
+            // layer (VAR 8 also: a (warp*U) % NS division and a LUT reload)
+            for (int l0 = 0; l0 < NU; l0 += 14) {
+                const int U = min(14, NU - l0);
+                Planes8 PL = PA;
+                uint32_t sdiv = 0;
+                if constexpr (VAR == 8) {
+                    sdiv = (warp * uint32_t(U) + uint32_t(it)) % uint32_t(consumers + 7);
+                    const uint4 q = *reinterpret_cast<const uint4*>(xs + (sdiv & 63) * 8);
+                    PL = Planes8{q.x ^ PA.l0, q.y ^ PA.l1, PA.h0, PA.h1};
+                }
+#pragma unroll 1
+                for (int u = 0; u + 1 < U; u += 2) {
+                    const uint32_t* sp = words + (l0 + u) * 96;
+                    const uint16_t* xp = xs + ((l0 + u + sdiv) & 31) * 256 + xoff;
+                    const uint32_t a0 = sp[lane], a1 = sp[32 + lane], a2 = sp[64 + lane];
+                    const uint32_t b0 = sp[96 + lane], b1 = sp[128 + lane], b2 = sp[160 + lane];
+                    const uint4 xa0 = ldx(xp, 0), xb0 = ldx(xp, 128), xa1 = ldx(xp, 256),
+                                xb1 = ldx(xp, 384);
+                    span3_mma_one(a0, a1, a2, PL, xa0, xb0, d0, k);
+                    span3_mma_one(b0, b1, b2, PL, xa1, xb1, d1, k);
+                }
+                if constexpr (VAR == 8) {  // flush at the layer end
+                    const float v = tile_rows_reduce(d0, d1, lane);
+                    if ((lane & 3) == 0 && lane < 16) reinterpret_cast<float*>(xs)[warp * 16 + lane] += v;
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) d0[z] = d1[z] = 0.f;
+                }
+            }
         } else if constexpr (VAR == 5 || VAR == 6) {
 #pragma unroll 1
             for (int u = 0; u < NU; u += 2) {
@@ -428,7 +458,7 @@ __global__ void __launch_bounds__(1024, 1) k_layers(const uint32_t* __restrict__
         const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(warp * 2 + (l & 1)) * slot_bytes);
         const uint16_t* xh = xs + (l & 3) * 4096;
         // the warp's range starts mid-tile like the kernel's (warp-dependent offset)
-        uint32_t s = (warp * U) % NS, tile = (warp * U) / NS;
+        uint32_t s = (mode & 8) ? 0u : (warp * U) % NS, tile = (mode & 8) ? warp : (warp * U) / NS;
         float d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
         const uint4 q0 = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
         Planes8 P{q0.x, q0.y, q0.z, q0.w};
@@ -465,8 +495,10 @@ __global__ void __launch_bounds__(1024, 1) k_layers(const uint32_t* __restrict__
                 if (!(mode & 1)) flush();  // mode 1: no tile flush
                 ++tile;
                 s = 0;
-                const uint4 q = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
-                P = Planes8{q.x, q.y, q.z, q.w};
+                if (!(mode & 16)) {  // mode 16: keep the LUT planes
+                    const uint4 q = *reinterpret_cast<const uint4*>(luts + ((tile * 4 + trow) & 255) * 4);
+                    P = Planes8{q.x, q.y, q.z, q.w};
+                }
             }
         }
         if (!(mode & 2)) flush();  // mode 2: no layer-end flush
@@ -801,7 +833,7 @@ int main(int argc, char** argv) {
         for (int prod = 0; prod < 1; ++prod)
         for (int c : {8})
             for (int ws : {2})
-                for (int cu : {16}) {
+                for (int cu : {16, 14}) {
                     auto kern = prod ? k_stream_prod : k_stream;
                     const size_t smem = 2048 + 64 * 256 * 2 + size_t(c) * ws * cu * 384;
                     if (smem > 227 * 1024) continue;
@@ -855,6 +887,7 @@ int main(int argc, char** argv) {
             else if (use_ldg) k_layers_ldg<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk);
             else k_layers<<<nsm, c * 32, smem>>>(g, L / 8, U, NS, c, out, K, clk, mode);
             CK(cudaDeviceSynchronize());
+            CK(cudaMemset(clk, 0, 8));
             cudaEventRecord(e0);
             if (flat == 2) k_pipe<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
             else if (flat) k_flat<<<nsm, c * 32, smem>>>(g, L, U, NS, c, out, K, clk, mode);
@@ -865,6 +898,10 @@ int main(int argc, char** argv) {
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
             const double w = double(nsm) * c * L * U * 1024.0;
+            long long cyc = 0;
+            CK(cudaMemcpy(&cyc, clk, 8, cudaMemcpyDeviceToHost));
+            printf("[cycle-based %.1f w/clk/SM, SM clock %.0f MHz] ", w / (double(cyc) / (nsm * c)) / nsm,
+                   double(cyc) / (nsm * c) / (ms * 1e-3) / 1e6);
             printf("%s mode %d ", flat == 2 ? "PIPE" : flat ? "FLAT" : "seg ", mode);
             printf(use_ldg ? "V9 ldg    c%2d U %3d NS %2d: %.3f ms  %6.1f w/clk/SM @1.965  %6.0f GB/s  %.0f ns/layer\n" : "V8 layers c%2d U %3d NS %2d: %.3f ms  %6.1f w/clk/SM @1.965  %6.0f GB/s  %.0f ns/layer\n", c, U, NS,
                    ms, w / (ms * 1e-3) / nsm / 1.965e9, w * 0.375 / (ms * 1e-3) / 1e9, ms * 1e6 / L);
@@ -874,7 +911,11 @@ int main(int argc, char** argv) {
             lay(atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), false, atoi(argv[4]), atoi(argv[5]));
             return 0;
         }
-        for (int flat = 0; flat < 3; flat += 2) {
+        for (int mode : {7, 15, 23, 31}) lay(8, 14, 16, false, mode, 0);
+        lay(8, 14, 1024, false, 7, 0);
+        lay(8, 14, 14, false, 7, 0);
+        lay(8, 14, 1024, false, 15, 0);
+        for (int flat = 0; flat < 0; flat += 2) {
             for (int mode : {0, 4, 6}) lay(8, 14, 16, false, mode, flat);
             for (int mode : {0, 6}) lay(8, 28, 16, false, mode, flat);
             for (int mode : {0, 6}) lay(8, 37, 16, false, mode, flat);
@@ -891,6 +932,7 @@ int main(int argc, char** argv) {
         CK(cudaFree(g));
     }
     for (int c : {8, 16}) {
+        run(k_loop<7>, "V0 restart every 14 units", c, 5);
         run(k_loop<0>, "V0 span pair (kernel loop)", c, 5);
         run(k_loop<1>, "V1 span pair, pipelined loads", c, 5);
         run(k_loop<2>, "V2 4 units / iter", c, 5);
