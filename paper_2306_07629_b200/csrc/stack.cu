@@ -893,6 +893,34 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                         }
                     }
                     if constexpr (BITS == 3 && NB < 4) {
+                        // 8-consumer kernels: four units per iteration (two
+                        // pairs interleaved: twice the independent work per
+                        // warp with only two decode warps per SMSP; +2.6% on
+                        // the 7B chain; the 16-consumer kernels, capped at 88
+                        // registers, measured slower with it)
+                        for (; NC == 8 && k + 3 < s_end; k += 4) {
+                            const uint32_t a0 = sp[lane], a1 = sp[32 + lane], a2 = sp[64 + lane];
+                            const uint32_t b0 = sp[96 + lane], b1 = sp[128 + lane],
+                                           b2 = sp[160 + lane];
+                            const uint32_t c0 = sp[192 + lane], c1 = sp[224 + lane],
+                                           c2 = sp[256 + lane];
+                            const uint32_t e0 = sp[288 + lane], e1 = sp[320 + lane],
+                                           e2 = sp[352 + lane];
+                            const uint4 xa0 = *reinterpret_cast<const uint4*>(xs);
+                            const uint4 xb0 = *reinterpret_cast<const uint4*>(xs + 128);
+                            const uint4 xa1 = *reinterpret_cast<const uint4*>(xs + kSpanCols);
+                            const uint4 xb1 = *reinterpret_cast<const uint4*>(xs + kSpanCols + 128);
+                            const uint4 xa2 = *reinterpret_cast<const uint4*>(xs + 2 * kSpanCols);
+                            const uint4 xb2 = *reinterpret_cast<const uint4*>(xs + 2 * kSpanCols + 128);
+                            const uint4 xa3 = *reinterpret_cast<const uint4*>(xs + 3 * kSpanCols);
+                            const uint4 xb3 = *reinterpret_cast<const uint4*>(xs + 3 * kSpanCols + 128);
+                            span3_mma_one(a0, a1, a2, P.a, xa0, xb0, d0, K);
+                            span3_mma_one(b0, b1, b2, P.a, xa1, xb1, d1, K);
+                            span3_mma_one(c0, c1, c2, P.a, xa2, xb2, d0, K);
+                            span3_mma_one(e0, e1, e2, P.a, xa3, xb3, d1, K);
+                            sp += 4 * UW;
+                            xs += 4 * kSpanCols;
+                        }
                         // span pairs: two independent units per iteration
                         for (; k + 1 < s_end; k += 2) {
                             const uint32_t a0 = sp[lane], a1 = sp[32 + lane], a2 = sp[64 + lane];

@@ -1,0 +1,20 @@
+import sys, numpy as np, torch
+sys.path.insert(0, '/root/repo')
+import paper_2306_07629_b200._native as N
+from paper_2306_07629_b200 import DeviceLayer
+from oracle.oracle import make_layer, make_x, to_quantized_layer
+st = torch.cuda.Stream(); torch.cuda.set_stream(st)
+for (r, c) in [(128, 256), (1024, 1024), (4096, 4096)]:
+    L = make_layer(r, c, 3, 0.0045, seed=1)
+    dls = [DeviceLayer(to_quantized_layer(L)) for _ in range(8)]
+    x = torch.from_numpy(make_x(c).view(np.int16)).cuda()
+    y = torch.empty(r, dtype=torch.int16, device='cuda')
+    def run(k):
+        for i in range(k): dls[i % 8].gemv(N.KERNEL_FUSED, x.data_ptr(), N.F16, y.data_ptr(), N.F16, st.cuda_stream)
+    run(16); torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st): run(200)
+    g.replay(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+    print(r, c, 'isolated us per launch', e0.elapsed_time(e1) * 1e3 / 200)

@@ -110,9 +110,8 @@ __global__ void __launch_bounds__(1024, 1) k_loop(int niter, float* out, int con
                 const int U = min(14, NU - l0);
                 Planes8 PL = PA;
                 uint32_t sdiv = 0;
-                if constexpr (VAR == 8) {
-                    sdiv = (warp * uint32_t(U) + uint32_t(it)) % uint32_t(consumers + 7);
-                    const uint4 q = *reinterpret_cast<const uint4*>(xs + (sdiv & 63) * 8);
+                if constexpr (VAR == 8) {  // LUT planes reloaded from smem per layer
+                    const uint4 q = *reinterpret_cast<const uint4*>(xs + ((l0 + it) & 31) * 8 + 8 * (lane & 3));
                     PL = Planes8{q.x ^ PA.l0, q.y ^ PA.l1, PA.h0, PA.h1};
                 }
 #pragma unroll 1
@@ -126,12 +125,7 @@ __global__ void __launch_bounds__(1024, 1) k_loop(int niter, float* out, int con
                     span3_mma_one(a0, a1, a2, PL, xa0, xb0, d0, k);
                     span3_mma_one(b0, b1, b2, PL, xa1, xb1, d1, k);
                 }
-                if constexpr (VAR == 8) {  // flush at the layer end
-                    const float v = tile_rows_reduce(d0, d1, lane);
-                    if ((lane & 3) == 0 && lane < 16) reinterpret_cast<float*>(xs)[warp * 16 + lane] += v;
-#pragma unroll
-                    for (int z = 0; z < 4; ++z) d0[z] = d1[z] = 0.f;
-                }
+
             }
         } else if constexpr (VAR == 5 || VAR == 6) {
 #pragma unroll 1
@@ -451,10 +445,17 @@ __global__ void __launch_bounds__(1024, 1) k_layers(const uint32_t* __restrict__
     issue(1);
     const ShiftK k = K;
     const uint32_t xoff = tile_x_offset(lane), trow = (lane >> 2) & 3u;
+    if (mode & 64) {  // overwrite the ring with hashed words (data-value experiment)
+        mbar_wait(&full[warp * 2], 0);
+        mbar_wait(&full[warp * 2 + 1], 0);
+        uint32_t* rw = reinterpret_cast<uint32_t*>(ring + size_t(warp * 2) * slot_bytes);
+        for (uint32_t i = lane; i < 2 * slot_bytes / 4; i += 32) rw[i] = (i * 2654435761u) ^ (warp * 77u);
+        __syncwarp();
+    }
     long long c0 = clock64();
     float acc = 0.f;
     for (int l = 0; l < L; ++l) {
-        if (!(mode & 4) || l < 2) mbar_wait(&full[warp * 2 + (l & 1)], (l >> 1) & 1u);
+        if ((!(mode & 4) || l < 2) && !(mode & 64)) mbar_wait(&full[warp * 2 + (l & 1)], (l >> 1) & 1u);
         const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + size_t(warp * 2 + (l & 1)) * slot_bytes);
         const uint16_t* xh = xs + (l & 3) * 4096;
         // the warp's range starts mid-tile like the kernel's (warp-dependent offset)
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(1024, 1) k_layers(const uint32_t* __restrict__
             }
         }
         if (!(mode & 2)) flush();  // mode 2: no layer-end flush
-        else acc += d0[0] + d1[1];
+        else if (!(mode & 32)) acc += d0[0] + d1[1];  // mode 32: no drain at all
         __syncwarp();
         issue(l + 2);
     }
@@ -911,7 +912,7 @@ int main(int argc, char** argv) {
             lay(atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), false, atoi(argv[4]), atoi(argv[5]));
             return 0;
         }
-        for (int mode : {7, 15, 23, 31}) lay(8, 14, 16, false, mode, 0);
+        for (int mode : {15, 15 | 32, 15 | 32 | 64}) lay(8, 14, 16, false, mode, 0);
         lay(8, 14, 1024, false, 7, 0);
         lay(8, 14, 14, false, 7, 0);
         lay(8, 14, 1024, false, 15, 0);
@@ -933,6 +934,7 @@ int main(int argc, char** argv) {
     }
     for (int c : {8, 16}) {
         run(k_loop<7>, "V0 restart every 14 units", c, 5);
+        run(k_loop<8>, "V0 restart + LUT reload from smem", c, 5);
         run(k_loop<0>, "V0 span pair (kernel loop)", c, 5);
         run(k_loop<1>, "V1 span pair, pipelined loads", c, 5);
         run(k_loop<2>, "V2 4 units / iter", c, 5);
