@@ -516,6 +516,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     }
     if world == 1 and not args.no_per_layer:
         line["per_layer"] = per_layer_bench(dev, peak)
+        line["model_stacks"] = model_stacks_bench(dev, peak)
+        line["batch_sweep"] = batch_sweep_bench(dev, peak)
     if world == 1 and not args.no_cpu_baseline:
         v, s, b, cores, desc = cpu_reference_sample(host_layers, args.ref_frac, repeats=3)
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": cores,
@@ -593,11 +595,112 @@ def per_layer_bench(dev, peak: float, launches: int = 200) -> dict:
     return out
 
 
+def model_stacks_bench(dev, peak: float, models=("13b", "65b"), tokens: int = 2) -> dict:
+    """BASELINE configs[2] / configs[3] (N = 1): whole LLaMA-13B / 65B linear
+    stacks (every decoder layer's 7 GEMVs, chained like the bench, 3-bit +
+    0.45% CSR, batch 1) as ONE persistent launch per `tokens` decode steps;
+    decoder layers rotate over distinct device weights totalling > 256 MB.
+    CUDA events on the launching stream."""
+    import torch
+    import paper_2306_07629_b200._native as N
+    from paper_2306_07629_b200 import DeviceLayer, DeviceStack
+    from paper_2306_07629_b200.tp import decoder_chain
+    from oracle.oracle import make_x, nnz_for
+    out = {}
+    st = torch.cuda.current_stream(dev)
+    for m in models:
+        h, f, n_dec = MODELS[m]
+        shapes = model_shapes(m)
+        cache = {}
+        qls = []
+        for _, r, c in shapes:
+            if (r, c) not in cache:
+                cache[(r, c)] = synthetic_layer(r, c, seed=r * 7 + c)
+            qls.append(cache[(r, c)])
+        dec_bytes = sum(int(N.lib.dsq_bytes_touched_estimate(r, c, BITS, 0,
+                                                            nnz_for(r * c, SPARSITY)))
+                        for _, r, c in shapes)
+        rot = max(2, -(-(256 << 20) // dec_bytes))
+        dls = [[DeviceLayer(q, device=dev.index or 0) for q in qls] for _ in range(rot)]
+        x = torch.from_numpy(make_x(h).view(np.int16)).to(dev)
+        ys = [[torch.empty(q.rows, dtype=torch.int16, device=dev) for q in qls] for _ in range(rot)]
+        deps, _, _ = decoder_chain(tokens * n_dec, 1)
+        layers, yp = [], []
+        for t in range(tokens * n_dec):
+            layers += dls[t % rot]
+            yp += [y.data_ptr() for y in ys[t % rot]]
+        stk = DeviceStack(layers, deps, [x.data_ptr() if d < 0 else 0 for d in deps], yp, N.F16)
+        stk.run(st.cuda_stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        stk.run(st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        gbs = dec_bytes * n_dec * tokens / (ms * 1e-3) / 1e9
+        out[f"llama{m}"] = {
+            "config": "BASELINE configs[2]" if m == "13b" else "BASELINE configs[3] (1 GPU)",
+            "decoder_layers": n_dec, "tokens": tokens, "ms_per_token": round(ms / tokens, 4),
+            "decode_tok_s_linear": round(tokens / (ms * 1e-3), 1),
+            "us_per_gemv": round(ms * 1e3 / (tokens * n_dec * 7), 3),
+            "GBs": round(gbs, 1), "frac": round(gbs / peak, 4), "rotation": rot,
+            "bytes_per_token": dec_bytes * n_dec}
+        del stk, dls
+        torch.cuda.synchronize()
+    return out
+
+
+def batch_sweep_bench(dev, peak: float, reps: int = 50) -> list:
+    """BASELINE configs[4] (a bounded slice): LLaMA-7B shapes, 3-bit + 0.45%,
+    batch 1/2/4/8/16, one fused product launch per batch (K7 with 2..8 vectors
+    sharing each decoded fragment, K8 beyond); bytes = weights once + the B
+    x / y vectors; layers rotate over > 256 MB."""
+    import torch
+    import paper_2306_07629_b200._native as N
+    from paper_2306_07629_b200 import DeviceLayer
+    from oracle.oracle import make_layer, make_x, to_quantized_layer
+    st = torch.cuda.current_stream(dev).cuda_stream
+    out = []
+    for rows, cols in [(4096, 4096), (11008, 4096)]:
+        L = make_layer(rows, cols, BITS, SPARSITY, seed=3)
+        q = to_quantized_layer(L)
+        wbytes = int(N.lib.dsq_bytes_touched_estimate(rows, cols, BITS, 0, L.nnz))
+        nl = max(2, -(-(256 << 20) // wbytes))
+        dls = [DeviceLayer(q, device=dev.index or 0) for _ in range(nl)]
+        base = None
+        for B in (1, 2, 4, 8, 16):
+            x = torch.from_numpy(np.stack([make_x(cols, seed=b) for b in range(B)])
+                                 .view(np.int16)).to(dev)
+            y = torch.empty(B, rows, dtype=torch.float16, device=dev)
+            for i in range(nl):
+                N.check(N.lib.dsq_cuda_gemv(dls[i].handle, N.KERNEL_FUSED, x.data_ptr(), N.F16,
+                                            y.data_ptr(), N.F16, B, st))
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(reps):
+                N.check(N.lib.dsq_cuda_gemv(dls[i % nl].handle, N.KERNEL_FUSED, x.data_ptr(),
+                                            N.F16, y.data_ptr(), N.F16, B, st))
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / reps
+            gbs = (wbytes + (B - 1) * (rows + cols) * 2) / us / 1e3
+            base = base or us
+            out.append({"shape": f"{rows}x{cols}", "batch": B, "us": round(us, 3),
+                        "GBs": round(gbs, 1), "frac": round(gbs / peak, 4),
+                        "speedup_vs_B_x_batch1": round(B * base / us, 2)})
+        del dls
+        torch.cuda.synchronize()
+    return out
+
+
 class TPUnavailable(RuntimeError):
     pass
 
 
-MODELS = {"7b": (4096, 11008, 32), "65b": (8192, 22016, 80)}  # hidden, ffn, decoder layers
+MODELS = {"7b": (4096, 11008, 32), "13b": (5120, 13824, 40),
+          "65b": (8192, 22016, 80)}  # hidden, ffn, decoder layers
 
 
 def model_shapes(model: str):
@@ -862,7 +965,7 @@ def main():
                          "TP path sizes its own rotation unless --no-rotation-auto)")
     ap.add_argument("--no-rotation-auto", dest="rotation_auto", action="store_false")
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of load before timing")
-    ap.add_argument("--workload", choices=["auto", "7b", "65b"], default="auto",
+    ap.add_argument("--workload", choices=["auto", "7b", "13b", "65b"], default="auto",
                     help="auto: the LLaMA-7B chain (configs[1]) at N=1, the 65B chain "
                          "tensor-parallel (configs[3]) at N>1")
     ap.add_argument("--multi", choices=["tp", "replicas"], default="tp",
@@ -873,7 +976,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-layer", action="store_true",
-                    help="skip the single-layer µs/layer section (configs[0], configs[1] shapes)")
+                    help="skip the per-layer (configs[0]/[1]), model-stack (configs[2]/[3] at "
+                         "N=1) and batch-sweep (configs[4]) sections")
     ap.add_argument("--ref-frac", type=float, default=1 / 16,
                     help="row fraction of each GEMV in the CPU sample")
     args = ap.parse_args()
