@@ -782,6 +782,10 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
                                                            q.sparse.nnz())) for q in shards)
     # rotation: distinct device weights per step totalling > 2x L2 per GPU
     n_rot = max(2, -(-(256 << 20) // shard_bytes)) if args.rotation_auto else args.rotation
+    if world > 1:  # every rank must run the same launch sequence
+        t = torch.tensor([n_rot], device=dev, dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n_rot = int(t.item())
     dls = [[DeviceLayer(q, device=local_rank) for q in shards] for _ in range(n_rot)]
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     ctx = None
