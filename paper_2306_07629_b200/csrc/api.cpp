@@ -212,7 +212,12 @@ uint32_t max_nnz_per_cta(const std::vector<uint32_t>& rp, uint32_t rows, int G) 
     return m;
 }
 
-constexpr uint64_t kSmallLayerUnits = 200;  // units per CTA below which 8 warps do a layer
+constexpr uint64_t kSmallLayerUnits = 200;  // (dev per-layer nca) units per CTA for 8 of 16 warps
+// 8 consumer warps (four units per iteration, 128 registers) while a CTA's
+// mean share of the stack's layers is at most this many units: the LLaMA-7B
+// chain (~190) and the 13B stack (~310, +1.5% over 16 warps); 16 warps for
+// the 65B stack (~780)
+constexpr uint64_t kEightWarpMeanUnits = 500;
 
 // dev (DSQ_STACK_NCA=1): 16-warp stacks whose small layers run on 8 of the
 // warps -- measured slower than an 8-warp kernel on the LLaMA-7B chain (2163
@@ -264,7 +269,7 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
         if (!per_layer_nca_enabled()) {  // the round-1 rule: mean units per layer
             uint64_t units = 0;
             for (uint32_t i = 0; i < n; ++i) units += uint64_t(ceil_div(Ls[i].tiles, G)) * Ls[i].ns;
-            sp.consumers = units <= kSmallLayerUnits * n ? 8u : kStackConsumersDefault;
+            sp.consumers = units <= kEightWarpMeanUnits * n ? 8u : kStackConsumersDefault;
         }
     }
     if (const char* e = std::getenv("DSQ_STACK_CONSUMERS")) {
