@@ -184,3 +184,23 @@ def test_shard_decoder_roles():
             else:
                 lo, hi = split_range(r, 2, rank, 32)
                 assert (s.rows, s.cols) == (hi - lo, c) and s.name.endswith(f".r{rank}")
+
+
+def test_split_range_and_shard_errors():
+    """dsq_split_range covers [0, n) with aligned, ordered, disjoint pieces;
+    the shard API rejects bad ranks and row-parallel grouped LUTs."""
+    import pytest as _pytest
+    from paper_2306_07629_b200 import DsqError
+    from paper_2306_07629_b200.tp import shard_cols, split_range
+    for n, world, align in [(4096, 8, 32), (22016, 8, 32), (11008, 3, 32), (100, 7, 1), (33, 4, 8)]:
+        pieces = [split_range(n, world, r, align) for r in range(world)]
+        assert pieces[0][0] == 0 and pieces[-1][1] == n
+        for (a, b), (c, d) in zip(pieces, pieces[1:]):
+            assert b == c and a <= b
+        assert all(lo % align == 0 for lo, _ in pieces)
+    with _pytest.raises(DsqError):
+        split_range(64, 2, 2, 32)  # rank >= world
+    q = to_quantized_layer(make_layer(8, 64, 3, 0.0, seed=1, groups=2))
+    with _pytest.raises(DsqError) as e:
+        shard_cols(q, 0, 2)
+    assert e.value.code == 102  # unsupported: grouped LUTs are channel-wise only here
