@@ -6,9 +6,9 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas 
 PKG       := paper_2306_07629_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libdsq_cuda.so
-OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
+OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/batch.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 
-all: $(LIB) oracle cxx-test
+all: $(LIB) oracle cxx-test plan-test
 
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/layout.hpp $(CSRC)/ptx.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/kernels.ptxas.log || (cat $(CSRC)/kernels.ptxas.log; false)
@@ -19,7 +19,10 @@ $(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layo
 $(CSRC)/batch.o: $(CSRC)/batch.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/batch.ptxas.log || (cat $(CSRC)/batch.ptxas.log; false)
 
-$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/layout.hpp $(CSRC)/stack.hpp include/dsq_cuda.h
+$(CSRC)/bstream.o: $(CSRC)/bstream.cu $(CSRC)/bstream.hpp $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/bstream.ptxas.log || (cat $(CSRC)/bstream.ptxas.log; false)
+
+$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/layout.hpp $(CSRC)/stack.hpp $(CSRC)/bstream.hpp include/dsq_cuda.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC,-fopenmp -c $< -o $@
 
 $(CSRC)/container.o: $(CSRC)/container.cpp include/dsq_cuda.h
@@ -50,7 +53,7 @@ PROFLIB := $(PKG)/libdsq_cuda_prof.so
 profile-lib: $(PROFLIB)
 $(CSRC)/stack_prof.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_PROFILE -c $< -o $@ 2> /dev/null
-$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
+$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 # debug variant: bounded waits that trap with the waiting site (stack.cu)
@@ -58,7 +61,7 @@ WDLIB := $(PKG)/libdsq_cuda_wd.so
 watchdog-lib: $(WDLIB)
 $(CSRC)/stack_wd.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_WATCHDOG -c $< -o $@
-$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/batch.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
+$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/batch.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 oracle:
@@ -79,11 +82,17 @@ cxx-test:
 	@echo "reference headers absent; using prebuilt $(CXXTEST) if present"
 endif
 
+# host-only check of K11's work plan (no GPU, no reference needed)
+PLANTEST := tests/cpp/test_bstream_plan
+plan-test: $(PLANTEST)
+$(PLANTEST): tests/cpp/test_bstream_plan.cpp $(CSRC)/bstream.o $(CSRC)/bstream.hpp
+	$(NVCC) $(ARCH) -std=c++17 -I$(CSRC) -o $@ $< $(CSRC)/bstream.o
+
 clean:
 	rm -f $(OBJS) $(LIB) $(CSRC)/*.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean cxx-test profile-lib watchdog-lib
+.PHONY: all oracle clean cxx-test plan-test profile-lib watchdog-lib
 
 # dev: A/B variants of the stack kernel (DSQ_CUDA_LIB=<lib> selects one)
 # make variant-lib VNAME=foo VFLAGS="-DFOO" -> paper_2306_07629_b200/libdsq_cuda_foo.so

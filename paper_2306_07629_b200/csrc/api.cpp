@@ -7,6 +7,8 @@
 // upload instead of inside every product (kernels.cpp:52,70,110).
 #include <cuda_runtime.h>
 
+#include "bstream.hpp"
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -409,6 +411,8 @@ struct dsq_cuda_layer {
     float* gseg8 = nullptr;
     cudaStream_t stream = nullptr;
     float* batch_part = nullptr;            // batched-product slice partials (lazy)
+    BStreamDevPlan bs[2] = {};              // K9 plans for B <= 8 / <= 16 (lazy)
+    void* bs_mem[2] = {nullptr, nullptr};   // their device allocations
     uint32_t batch_kslices = 0, batch_spans = 0;
     std::mutex mu;       // guards dense_w materialization and batch_part
     std::mutex host_mu;  // serializes the host-buffer API on the internal stream
@@ -890,6 +894,8 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (L->y32_pin) cudaFreeHost(L->y32_pin);
     if (L->dense_w) cudaFree(L->dense_w);
     if (L->batch_part) cudaFree(L->batch_part);
+    for (void* m : L->bs_mem)
+        if (m) cudaFree(m);
     if (L->gseg2) cudaFree(L->gseg2);
     if (L->gseg4) cudaFree(L->gseg4);
     if (L->gseg8) cudaFree(L->gseg8);
@@ -928,7 +934,67 @@ static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
     return DSQ_OK;
 }
 
-// batched products (K8, batch.cu): x [batch][cols] fp16, y [batch][rows]
+// which kernel runs a batched product: K7 (the persistent batch-1 kernel with
+// NB = 2 / 4 / 8 vectors per decoded fragment) for batch 2..4, K11 (bstream.cu:
+// dense fragment map on per-warp TMA rings) for 5..16 and for batches whose x
+// does not fit next to K7's ring.  DSQ_BATCH_PATH=k7 / k8 selects K7 (up to
+// batch 8) or the older K8 (batch.cu) instead, for A/B measurements.
+enum class BatchRoute { k7, k8, k11 };
+static BatchRoute batch_route(const dsq_cuda_layer* L, uint32_t batch) {
+    static const int forced = [] {
+        const char* e = std::getenv("DSQ_BATCH_PATH");
+        return !e ? 0 : !std::strcmp(e, "k7") ? 7 : !std::strcmp(e, "k8") ? 8 : 0;
+    }();
+    const uint32_t nbk = batch == 2 ? 2u : batch <= 4 ? 4u : 8u;
+    if (forced == 8 && batch > 4) return BatchRoute::k8;
+    if ((batch <= 4 || (forced == 7 && batch <= 8)) && !L->k7_batch_failed(nbk))
+        return BatchRoute::k7;
+    return forced == 8 ? BatchRoute::k8 : BatchRoute::k11;
+}
+
+// K11's plan for B <= 8 * nb vectors: warp ranges, segment numbering, the
+// segment partials and the transposed x (caller holds L->mu)
+static int ensure_bstream(dsq_cuda_layer* L, uint32_t nb) {
+    if (L->bs_mem[nb - 1]) return DSQ_OK;
+    const BStreamPlanHost h = bstream_plan(L->tiles, L->ns, L->bits, nb, uint32_t(L->num_sms));
+    const size_t smem = bstream_smem_bytes(L->bits, nb, h.max_span, h.cs);
+    if (smem > 232448 || h.phases > 255)
+        return fail(DSQ_E_UNSUPPORTED, "batched plan: %zu bytes of shared memory, %u phases", smem,
+                    h.phases);
+    auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t b_w = up(h.wdesc.size() * 4), b_s = up(h.seg_base.size() * 4),
+                 b_p = up(h.phase_span.size() * 4), b_part = up(size_t(h.nseg) * 16 * 8 * nb * 4),
+                 b_xt = up(size_t(L->ns) * kSpanCols * 8 * nb * 2);
+    uint8_t* m = nullptr;
+    CUDA_TRY(cudaMalloc(&m, b_w + b_s + b_p + b_part + b_xt));
+    BStreamDevPlan& d = L->bs[nb - 1];
+    d.phases = h.phases;
+    d.nseg = h.nseg;
+    d.max_span = h.max_span;
+    d.cs = h.cs;
+    d.grid = h.grid;
+    d.tiles16 = (L->tiles + 3) / 4;
+    d.wdesc = reinterpret_cast<uint4*>(m);
+    d.seg_base = reinterpret_cast<uint32_t*>(m + b_w);
+    d.phase_span = reinterpret_cast<uint32_t*>(m + b_w + b_s);
+    d.part = reinterpret_cast<float*>(m + b_w + b_s + b_p);
+    d.xT = reinterpret_cast<uint16_t*>(m + b_w + b_s + b_p + b_part);
+    cudaError_t e = cudaMemcpy(d.wdesc, h.wdesc.data(), h.wdesc.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(d.seg_base, h.seg_base.data(), h.seg_base.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(d.phase_span, h.phase_span.data(), h.phase_span.size() * 4,
+                       cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(m);
+        return cuda_fail(e, "batched plan upload");
+    }
+    L->bs_mem[nb - 1] = m;
+    return DSQ_OK;
+}
+
+// batched products on K11 (bstream.cu) or K8 (batch.cu): x [batch][cols]
+// fp16, y [batch][rows]
 static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype, void* y,
                       int y_dtype, uint32_t batch, cudaStream_t st, uint32_t x_stride,
                       uint32_t y_stride) {
@@ -941,6 +1007,19 @@ static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype,
         return fail(DSQ_E_INVALID_ARGUMENT, "batched x rows must be 16-byte aligned (stride %% 8 == 0)");
     if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
         return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
+    const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
+    if (batch_route(L, batch) != BatchRoute::k8) {
+        const uint32_t nb = batch > 8 ? 2u : 1u;
+        {
+            std::lock_guard<std::mutex> lk(L->mu);
+            const int rc = ensure_bstream(L, nb);
+            if (rc) return rc;
+        }
+        CUDA_TRY(launch_bstream(L->bits, nb, L->bs[nb - 1], L->rec, L->tlut, L->P.row_ptr, L->P.csr,
+                                L->rows, L->cols, L->ns, L->tiles, static_cast<const uint16_t*>(x),
+                                x_stride, batch, y, y_stride, y_dtype == DSQ_F16, mode, st));
+        return DSQ_OK;
+    }
     {
         std::lock_guard<std::mutex> lk(L->mu);
         if (!L->batch_part) {
@@ -957,7 +1036,6 @@ static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype,
                                     size_t(L->ns) * kSpanCols * 16 * sizeof(uint16_t)));
         }
     }
-    const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
     CUDA_TRY(launch_batch(L->bits, L->rec, L->tlut, L->P.row_ptr, L->P.csr, L->rows, L->cols,
                           L->ns, L->tiles, static_cast<const uint16_t*>(x), x_stride, batch, y,
                           y_stride, y_dtype == DSQ_F16, L->batch_part, L->batch_kslices,
@@ -1002,7 +1080,7 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
     if (L->grouped && batch > 1)
         return fail(DSQ_E_UNSUPPORTED, "grouped LUTs: batched reference kernel");
     const uint32_t nbk = batch == 2 ? 2u : batch <= 4 ? 4u : 8u;
-    if (batch >= 2 && batch <= 8 && L->rec_layout && !L->k7_batch_failed(nbk) &&
+    if (batch >= 2 && batch <= 8 && L->rec_layout && batch_route(L, batch) == BatchRoute::k7 &&
         (kernel == DSQ_KERNEL_LUT || kernel == DSQ_KERNEL_FUSED) &&
         x_dtype == DSQ_F16 && (y_dtype == DSQ_F32 || y_dtype == DSQ_F16) &&
         !(reinterpret_cast<uintptr_t>(x) & 15u) && x_stride % 8 == 0) {
@@ -1771,8 +1849,7 @@ int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
                                      S->batch, static_cast<cudaStream_t>(stream), true,
                                      q.x_stride, q.y_stride);
             if (rc) return rc;
-            const uint32_t nbk = S->batch == 2 ? 2u : S->batch <= 4 ? 4u : 8u;
-            launches += S->batch == 1 || (S->batch <= 8 && !q.layer->k7_batch_failed(nbk)) ? 1u : 2u;
+            launches += S->batch == 1 || batch_route(q.layer, S->batch) == BatchRoute::k7 ? 1u : 2u;
         }
         S->launches = launches;
         return DSQ_OK;

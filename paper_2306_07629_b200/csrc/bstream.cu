@@ -1,0 +1,496 @@
+// bstream.cu -- K11: batched Dense-and-Sparse LUT-GEMM Y[b] = W X[b] for
+// B = 5..16 activation vectors (BASELINE configs[4]) on per-warp TMA rings.
+//
+// Same HBM layout as the batch-1 kernel (stack.hpp: 4-row tiles, 256-column
+// spans) read with the DENSE fragment map of K8 (batch.cu): a warp decodes a
+// 16-row tile (4 consecutive 4-row tiles) and every mma.sync.m16n8k16 uses all
+// 16 A rows and all 8 B columns = 8 batch vectors, so one decoded weight feeds
+// up to 16 products for the tensor cost of batch 1 (B <= 8: 4 HMMA per 1024
+// weights, as the batch-1 block-diagonal map; B <= 16: 8).
+//
+// Work split (host plan, bstream_plan below).  The columns are cut in PHASES
+// of at most 8 (B > 8) or 16 spans, so one phase's x for all 8*NB vectors is
+// 64 KB of shared memory; a CELL is (16-row tile q, span s) of a phase, ordered
+// q-major.  Every CTA works in one phase on a contiguous cell range (CTAs per
+// phase in proportion to the phase's cells), split again into 8 contiguous
+// warp ranges.  Each warp streams its range through a private ring of 3 slots:
+// a slot holds one CHUNK = up to cs consecutive spans of one 16-row tile, i.e.
+// 4 bulk copies (one per 4-row tile, each a contiguous run of units) plus the
+// tile's LUT planes, completed on one mbarrier.  The copies for the first
+// three chunks are issued before the PDL wait (the weights are immutable), the
+// phase's x is staged once per CTA after it.
+//
+// A warp flushes its accumulators when its range leaves a 16-row tile: one
+// SEGMENT = the warp's partial products of that tile's 16 rows x 8*NB vectors
+// (1 KB at NB = 2).  The host numbers the segments so that those of tile q,
+// phase p are seg_base[p*T + q] .. seg_base[p*T + q + 1]; bstream_finish sums
+// them in that fixed order, adds the CSR deltas, and writes y (deterministic,
+// no atomics).  Segments cost ~(T*phases + warps) KB of L2-resident traffic,
+// a few percent of the weight bytes at 7B shapes.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "bstream.hpp"
+#include "ptx.cuh"
+#include "stack.hpp"
+#include "tile.cuh"
+
+namespace sqz {
+
+constexpr int kBsWarps = 8;
+constexpr int kBsSlots = 3;
+constexpr uint32_t kBsBarBytes = 256;  // mbarrier area at the start of shared memory
+
+struct BStreamParams {
+    const uint32_t* idx;         // [tiles4][ns][UW]
+    const uint32_t* lut;         // [tiles4][4][LW]
+    const uint16_t* x;           // [B][x_stride] fp16, rows 16-byte aligned
+    float* part;                 // [nseg][16][8*NB] segment partials
+    uint16_t* xT;                // [ns*256][8*NB] x transposed for the CSR pass (or null)
+    const uint4* wdesc;          // [grid*8] {cell_begin, cell_end, seg_first, bs_pack_w(phase, a, gp)}
+    const uint32_t* seg_base;    // [phases*tiles16 + 1]
+    const uint32_t* phase_span;  // [phases + 1] span boundaries
+    uint32_t cols, ns, tiles4, tiles16, B, x_stride;
+    uint32_t xs_stride;    // halves per staged x row (max phase spans * 256 + 32)
+    uint32_t cs;           // spans per chunk
+    // slot layout (words): 4-row tiles 0, 1 at 0 and pw, the LUT planes of
+    // all four at pw + cs*UW, tiles 2, 3 at pair and pair + pw.  pw = cs*UW +
+    // 16 = 16 mod 32 keeps the two tiles one instruction reads on opposite
+    // bank halves.
+    uint32_t pw, pair, lut_off, slot_words;
+};
+
+// wdesc .w: phase (bits 0..7) | the CTA's index among the phase's CTAs
+// (bits 8..19) | the phase's CTA count (bits 20..31) -- the CTAs of a phase
+// write its transposed x between them
+SQZ_HD inline uint32_t bs_pack_w(uint32_t phase, uint32_t a, uint32_t gp) {
+    return phase | (a << 8) | (gp << 20);
+}
+
+// lane_quads / quad_col: batch.cu
+template <int BITS>
+__device__ __forceinline__ void bs_quads(const uint32_t* w, uint32_t (&q)[8], uint32_t (&pk)[8]) {
+    if constexpr (BITS == 3) {
+        const uint32_t m0 = w[0] & 0x77777777u, m1 = w[1] & 0x77777777u, m2 = w[2] & 0x77777777u;
+        const uint32_t t = ((w[0] >> 3) & 0x11111111u) | ((w[1] >> 2) & 0x22222222u) |
+                           ((w[2] >> 1) & 0x44444444u);
+        q[0] = m0; q[1] = hi16(m0); q[2] = m1; q[3] = hi16(m1);
+        q[4] = m2; q[5] = hi16(m2); q[6] = t; q[7] = hi16(t);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t sl = w[k] & 0x77777777u;
+            const uint32_t p = ((w[k] >> 1) & 0x44444444u) | 0x32103210u;
+            q[2 * k] = sl;
+            q[2 * k + 1] = hi16(sl);
+            pk[2 * k] = p;
+            pk[2 * k + 1] = hi16(p);
+        }
+    }
+}
+
+// one cell (16-row tile x one span) from the ring slot: u0 / u1 = the span's
+// unit of the lane's 4-row tiles j0 / j0 + 2.  x B fragments: one LDS.128
+// covers quads qi and qi + 1 (8 consecutive columns); with the staged rows
+// 32 halves off a 64-half boundary the 8 lanes of each quarter-warp hit 32
+// distinct banks.
+template <int BITS, int NB>
+__device__ __forceinline__ void bs_cell(const uint32_t* u0, const uint32_t* u1, uint32_t xcol,
+                                        uint32_t i, uint32_t t, const Planes16& P0,
+                                        const Planes16& P1, const uint16_t* xg0,
+                                        const uint16_t* xg1, float (&d)[2][NB][4]) {
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t L = 16 * h + 4 * i + t;
+        uint32_t w0[BITS], w1[BITS];
+        if constexpr (BITS == 3) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                w0[k] = u0[k * 32 + L];
+                w1[k] = u1[k * 32 + L];
+            }
+        } else {
+            const uint4 a = *reinterpret_cast<const uint4*>(u0 + L * 4);
+            const uint4 b = *reinterpret_cast<const uint4*>(u1 + L * 4);
+            w0[0] = a.x; w0[1] = a.y; w0[2] = a.z; w0[3] = a.w;
+            w1[0] = b.x; w1[1] = b.y; w1[2] = b.z; w1[3] = b.w;
+        }
+        uint32_t q0[8], q1[8], k0[8], k1[8];
+        bs_quads<BITS>(w0, q0, k0);
+        bs_quads<BITS>(w1, q1, k1);
+#pragma unroll
+        for (uint32_t qp = 0; qp < 8; qp += 2) {
+            const uint32_t col = xcol + tile_col(h, t, qp < 4 ? 4 * qp : 16 + 4 * (qp - 4));
+            const uint4 xb = *reinterpret_cast<const uint4*>(xg0 + col);
+            uint4 xc;
+            if constexpr (NB == 2) xc = *reinterpret_cast<const uint4*>(xg1 + col);
+#pragma unroll
+            for (uint32_t e = 0; e < 2; ++e) {
+                const uint32_t qi = qp + e;
+                uint32_t a0, a1, a2, a3;
+                if constexpr (BITS == 3) {
+                    quad8(q0[qi], P0.a, a0, a2);
+                    quad8(q1[qi], P1.a, a1, a3);
+                } else {
+                    quad16(q0[qi], k0[qi], P0, a0, a2);
+                    quad16(q1[qi], k1[qi], P1, a1, a3);
+                }
+                hmma16816(d[h][0], a0, a1, a2, a3, e ? xb.z : xb.x, e ? xb.w : xb.y);
+                if constexpr (NB == 2)
+                    hmma16816(d[h][NB - 1], a0, a1, a2, a3, e ? xc.z : xc.x, e ? xc.w : xc.y);
+            }
+        }
+    }
+}
+
+template <int BITS, int NB>  // NB = HMMA column groups (1: B <= 8, 2: B <= 16)
+__global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_constant__ BStreamParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t LW = BITS == 3 ? 4u : 8u;
+    constexpr uint32_t UW = BITS * 32u;
+    constexpr uint32_t NBV = 8u * NB;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp * kBsSlots;
+    uint32_t* ring = reinterpret_cast<uint32_t*>(smem + kBsBarBytes) + warp * kBsSlots * p.slot_words;
+    uint16_t* xs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint32_t*>(smem + kBsBarBytes) +
+                                               kBsWarps * kBsSlots * p.slot_words);
+    const uint4 wd = p.wdesc[blockIdx.x * kBsWarps + warp];
+    const uint32_t phase = wd.w & 0xffu;
+    const uint32_t sa = p.phase_span[phase], S = p.phase_span[phase + 1] - sa;
+    const uint32_t cb = wd.x, ce = wd.y;
+    // chunk at cell c: 16-row tile q = c / S, phase-local span c % S, up to cs
+    // spans, not past the tile's last span or the warp's range
+    auto issue = [&](uint32_t c, uint32_t slot, uint64_t pol) -> uint32_t {
+        const uint32_t q = c / S, sl = c - q * S;
+        const uint32_t n = min(min(p.cs, S - sl), ce - c);
+        const uint32_t nt = min(4u, p.tiles4 - 4 * q);  // 4-row tiles that exist
+        uint32_t* dst = ring + slot * p.slot_words;
+        mbar_arrive_expect_tx(bar + slot, nt * (16u * LW + n * UW * 4u));
+        bulk_g2s(dst + p.lut_off, p.lut + size_t(4 * q) * kTileRows * LW, nt * kTileRows * LW * 4u, bar + slot,
+                 pol);
+        for (uint32_t j = 0; j < nt; ++j)
+            bulk_g2s(dst + (j & 1) * p.pw + (j >> 1) * p.pair,
+                     p.idx + (size_t(4 * q + j) * p.ns + sa + sl) * UW, n * UW * 4u, bar + slot, pol);
+        return c + n;
+    };
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(smem) + kBsWarps * kBsSlots;
+    uint32_t c_issue = cb;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kBsSlots; ++s) mbar_init(bar + s, 1);
+        if (warp == 0) mbar_init(xbar, 1);
+        fence_barrier_init();
+        const uint64_t pol = policy_evict_first();
+        for (int s = 0; s < kBsSlots && c_issue < ce; ++s) c_issue = issue(c_issue, s, pol);
+    }
+    // x, the segment buffer and xT may belong to the previous launch on this
+    // stream (programmatic dependent launch): wait before touching them
+    pdl_trigger();
+    pdl_wait();
+    {
+        // the phase's x: the 16-byte-aligned body of each live vector row by
+        // bulk copies on xbar (thread 0), the ragged tail and the rows of
+        // vectors >= B by plain stores (disjoint bytes)
+        const uint32_t c0 = sa * kSpanCols;
+        const uint32_t ccount = min(p.cols, (sa + S) * kSpanCols) - min(p.cols, c0);
+        const uint32_t body = ccount & ~7u;  // halves copied by TMA per row
+        const uint32_t nlive = min(p.B, NBV);
+        __syncthreads();  // xbar initialised
+        if (threadIdx.x == 0) {
+            mbar_arrive_expect_tx(xbar, nlive * body * 2u);
+            if (body)
+                for (uint32_t b = 0; b < nlive; ++b)
+                    bulk_g2s_plain(xs + b * p.xs_stride, p.x + size_t(b) * p.x_stride + c0, body * 2u,
+                                   xbar);
+        }
+        const uint32_t rowh = S * kSpanCols;  // staged halves per row
+        for (uint32_t b = warp; b < NBV; b += kBsWarps) {
+            const uint32_t from = b < nlive ? body : 0u;
+            for (uint32_t c = from + lane; c < rowh; c += 32)
+                xs[b * p.xs_stride + c] = b < nlive && c < ccount ? p.x[size_t(b) * p.x_stride + c0 + c]
+                                                                  : uint16_t(0);
+        }
+        __syncthreads();
+        mbar_wait_spin(xbar, 0);
+        if (p.xT) {
+            // this CTA's share of the phase's transposed x: all vectors of a
+            // column in one 16- / 32-byte run for the CSR gathers
+            const uint32_t a = (wd.w >> 8) & 0xfffu, gp = wd.w >> 20;
+            const uint32_t x0 = uint32_t(uint64_t(ccount) * a / gp);
+            const uint32_t x1 = uint32_t(uint64_t(ccount) * (a + 1) / gp);
+            for (uint32_t k = x0 * NB + threadIdx.x; k < x1 * NB; k += blockDim.x) {
+                const uint32_t c = k / NB, j = k - c * NB;
+                uint32_t h[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    h[e] = uint32_t(xs[(8 * j + 2 * e) * p.xs_stride + c]) |
+                           (uint32_t(xs[(8 * j + 2 * e + 1) * p.xs_stride + c]) << 16);
+                *reinterpret_cast<uint4*>(p.xT + size_t(c0 + c) * NBV + 8 * j) =
+                    make_uint4(h[0], h[1], h[2], h[3]);
+            }
+        }
+    }
+    if (cb >= ce) return;
+    const uint32_t g = lane >> 2, t = lane & 3, i = g & 3, j0 = g >> 2;  // rows g, g+8: tiles j0, j0+2
+    const uint16_t* xg0 = xs + g * p.xs_stride;        // vector g
+    const uint16_t* xg1 = xs + (8 + g) * p.xs_stride;  // vector 8 + g (NB == 2)
+    float d[2][NB][4];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int n = 0; n < NB; ++n) d[c][n][0] = d[c][n][1] = d[c][n][2] = d[c][n][3] = 0.f;
+    uint32_t seg = wd.z;
+    uint32_t it = 0;
+    for (uint32_t c = cb; c < ce;) {
+        const uint32_t q = c / S, sl = c - q * S;
+        const uint32_t n = min(min(p.cs, S - sl), ce - c);
+        const uint32_t slot = it % kBsSlots;
+        mbar_wait_spin(bar + slot, (it / kBsSlots) & 1u);
+        const uint32_t* sw = ring + slot * p.slot_words;
+        const bool v0 = 4 * q + j0 < p.tiles4, v1 = 4 * q + j0 + 2 < p.tiles4;
+        Planes16 P0, P1;
+        {
+            const uint32_t* lt = sw + p.lut_off;
+            const uint4 a0 = *reinterpret_cast<const uint4*>(lt + (j0 * 4 + i) * LW);
+            const uint4 a1 = *reinterpret_cast<const uint4*>(lt + ((j0 + 2) * 4 + i) * LW);
+            P0.a = v0 ? Planes8{a0.x, a0.y, a0.z, a0.w} : Planes8{0u, 0u, 0u, 0u};
+            P1.a = v1 ? Planes8{a1.x, a1.y, a1.z, a1.w} : Planes8{0u, 0u, 0u, 0u};
+            if constexpr (BITS == 4) {
+                const uint4 b0 = *reinterpret_cast<const uint4*>(lt + (j0 * 4 + i) * LW + 4);
+                const uint4 b1 = *reinterpret_cast<const uint4*>(lt + ((j0 + 2) * 4 + i) * LW + 4);
+                P0.b = v0 ? Planes8{b0.x, b0.y, b0.z, b0.w} : Planes8{0u, 0u, 0u, 0u};
+                P1.b = v1 ? Planes8{b1.x, b1.y, b1.z, b1.w} : Planes8{0u, 0u, 0u, 0u};
+            }
+        }
+        const uint32_t* u0 = sw + j0 * p.pw;
+        const uint32_t* u1 = u0 + p.pair;
+        uint32_t u = 0;
+        for (; u + 2 <= n; u += 2, u0 += 2 * UW, u1 += 2 * UW) {  // two spans: independent chains
+            bs_cell<BITS, NB>(u0, u1, (sl + u) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
+            bs_cell<BITS, NB>(u0 + UW, u1 + UW, (sl + u + 1) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
+        }
+        if (u < n) bs_cell<BITS, NB>(u0, u1, (sl + u) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
+        // the slot's words are in registers or consumed: refill it
+        __syncwarp();
+        if (lane == 0 && c_issue < ce) c_issue = issue(c_issue, slot, policy_evict_first());
+        ++it;
+        c += n;
+        if (c == ce || c - q * S == S) {
+            // the range leaves tile q: one segment = D rows g / g+8, vectors 8n + 2t, +1
+            float* out = p.part + size_t(seg) * 16 * NBV;
+#pragma unroll
+            for (int nn = 0; nn < NB; ++nn) {
+                const uint32_t b0 = 8 * nn + 2 * t;
+                *reinterpret_cast<float2*>(out + g * NBV + b0) =
+                    make_float2(d[0][nn][0] + d[1][nn][0], d[0][nn][1] + d[1][nn][1]);
+                *reinterpret_cast<float2*>(out + (g + 8) * NBV + b0) =
+                    make_float2(d[0][nn][2] + d[1][nn][2], d[0][nn][3] + d[1][nn][3]);
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) d[cc][nn][0] = d[cc][nn][1] = d[cc][nn][2] = d[cc][nn][3] = 0.f;
+            }
+            // a later tile of this range starts with this warp: its first segment
+            if (c < ce) seg = p.seg_base[phase * p.tiles16 + q + 1];
+        }
+    }
+}
+
+// y[b][r] = sum of the row's segments (phase by phase, in segment order) +
+// its CSR deltas.  One warp per row: lane = part * XB + b (XB = 8 * NB), the
+// CSR entries split over the 32 / XB parts in groups of 8 and added in a fixed
+// shuffle order, as batch_finish (batch.cu).
+template <int XB>
+__global__ void bstream_finish(const float* __restrict__ part, const uint32_t* __restrict__ seg_base,
+                               uint32_t phases, uint32_t tiles16, uint32_t rows, uint32_t B,
+                               const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
+                               const uint16_t* __restrict__ x, uint32_t x_stride,
+                               const uint16_t* __restrict__ xT, void* y, uint32_t y_stride,
+                               int y_f16, int with_dense, int with_csr) {
+    constexpr uint32_t P = 32 / XB;
+    pdl_trigger();
+    pdl_wait();  // the segments of the preceding bstream_gemv
+    const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31, b = lane % XB, k = lane / XB;
+    if (r >= rows) return;  // whole warps
+    const bool live = b < B;
+    float s = 0.f;
+    if (with_csr && live) {
+        const uint16_t* xb = xT ? xT + b : x + size_t(b) * x_stride;
+        const uint32_t xs = xT ? uint32_t(XB) : 1u;
+        const uint32_t q0 = row_ptr[r], q1 = row_ptr[r + 1];
+        for (uint32_t q = q0 + 8 * k; q < q1; q += 8 * P) {
+            uint32_t e[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) e[u] = q + u < q1 ? __ldg(csr + q + u) : 0u;
+            uint16_t xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                xv[u] = q + u < q1 ? __ldg(xb + size_t(e[u] & 0xffffu) * xs) : uint16_t(0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (q + u < q1) s = fma_h(uint16_t(e[u] >> 16), xv[u], s);
+        }
+    }
+#pragma unroll
+    for (uint32_t o = XB; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (k != 0 || !live) return;
+    if (with_dense) {
+        const uint32_t q = r >> 4, rr = r & 15u;
+        float dsum = 0.f;
+        for (uint32_t ph = 0; ph < phases; ++ph) {
+            const uint32_t s0 = seg_base[ph * tiles16 + q], s1 = seg_base[ph * tiles16 + q + 1];
+            for (uint32_t sg = s0; sg < s1; ++sg) dsum += part[(size_t(sg) * 16 + rr) * XB + b];
+        }
+        s = dsum + s;
+    }
+    if (y_f16)
+        static_cast<__half*>(y)[size_t(b) * y_stride + r] = __float2half_rn(s);
+    else
+        static_cast<float*>(y)[size_t(b) * y_stride + r] = s;
+}
+
+template <class K, class... A>
+static cudaError_t launch_pdl_bs(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// ---- host plan -------------------------------------------------------------
+
+
+// Split a layer (tiles4 4-row tiles, ns spans) for B <= 8 * nb vectors over
+// `grid` CTAs.  Pure host arithmetic (unit-tested through the C ABI).
+BStreamPlanHost bstream_plan(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32_t nb,
+                             uint32_t grid) {
+    BStreamPlanHost pl;
+    const uint32_t T = (tiles4 + 3) / 4;
+    const uint32_t smax = nb == 2 ? 8u : 16u;  // 64 KB of staged x per phase
+    const uint32_t P = std::max<uint32_t>(1, (ns + smax - 1) / smax);  // <= 255 (wdesc .w)
+    pl.phases = P;
+    pl.phase_span.resize(P + 1);
+    for (uint32_t k = 0; k <= P; ++k) pl.phase_span[k] = uint32_t(uint64_t(k) * ns / P);
+    for (uint32_t k = 0; k < P; ++k)
+        pl.max_span = std::max(pl.max_span, pl.phase_span[k + 1] - pl.phase_span[k]);
+    pl.cs = bits == 3 ? 4u : 3u;
+    grid = std::max(grid, P);
+    pl.grid = grid;
+    // CTAs per phase in proportion to the phase's spans (>= 1 each)
+    std::vector<uint32_t> gp(P);
+    uint32_t used = 0;
+    for (uint32_t k = 0; k < P; ++k) {
+        const uint32_t sp = pl.phase_span[k + 1] - pl.phase_span[k];
+        gp[k] = std::max<uint32_t>(1, uint32_t(uint64_t(grid) * sp / ns));
+        used += gp[k];
+    }
+    // floor(grid * sp / ns) >= 1 for balanced phases, so used <= grid here
+    for (uint32_t k = 0; used < grid; k = (k + 1) % P, ++used) ++gp[k];
+    // warp ranges, then segment counts per (phase, tile16)
+    pl.wdesc.assign(size_t(grid) * kBsWarps * 4, 0);
+    std::vector<uint32_t> pieces(size_t(P) * T, 0);
+    uint32_t cta = 0;
+    for (uint32_t k = 0; k < P; ++k) {
+        const uint32_t S = pl.phase_span[k + 1] - pl.phase_span[k];
+        const uint64_t C = uint64_t(T) * S;
+        for (uint32_t a = 0; a < gp[k]; ++a, ++cta) {
+            const uint64_t cb = C * a / gp[k], ce = C * (a + 1) / gp[k];
+            for (uint32_t w = 0; w < uint32_t(kBsWarps); ++w) {
+                const uint32_t wb = uint32_t(cb + (ce - cb) * w / kBsWarps);
+                const uint32_t we = uint32_t(cb + (ce - cb) * (w + 1) / kBsWarps);
+                uint32_t* d = &pl.wdesc[(size_t(cta) * kBsWarps + w) * 4];
+                d[0] = wb;
+                d[1] = we;
+                d[3] = bs_pack_w(k, a, gp[k]);
+                if (wb < we)
+                    for (uint32_t q = wb / S; q <= (we - 1) / S; ++q) ++pieces[size_t(k) * T + q];
+            }
+        }
+    }
+    pl.seg_base.assign(size_t(P) * T + 1, 0);
+    for (size_t z = 0; z < size_t(P) * T; ++z) pl.seg_base[z + 1] = pl.seg_base[z] + pieces[z];
+    pl.nseg = pl.seg_base[size_t(P) * T];
+    // each warp's first segment: seg_base of its first tile + the earlier warps on that tile
+    std::vector<uint32_t> seen(size_t(P) * T, 0);
+    for (uint32_t c = 0; c < grid; ++c)
+        for (uint32_t w = 0; w < uint32_t(kBsWarps); ++w) {
+            uint32_t* d = &pl.wdesc[(size_t(c) * kBsWarps + w) * 4];
+            const uint32_t k = d[3] & 0xffu;
+            const uint32_t S = pl.phase_span[k + 1] - pl.phase_span[k];
+            if (d[0] >= d[1]) continue;
+            const uint32_t q0 = d[0] / S, q1 = (d[1] - 1) / S;
+            d[2] = pl.seg_base[size_t(k) * T + q0] + seen[size_t(k) * T + q0];
+            for (uint32_t q = q0; q <= q1; ++q) ++seen[size_t(k) * T + q];
+        }
+    return pl;
+}
+
+size_t bstream_smem_bytes(uint32_t bits, uint32_t nb, uint32_t max_span, uint32_t cs) {
+    const uint32_t LW = bits == 3 ? 4u : 8u, UW = bits * 32u;
+    const size_t slot = 2u * (cs * UW + 16u) + 2u * cs * UW + 16u * LW;  // BStreamParams
+    return kBsBarBytes + size_t(kBsWarps) * kBsSlots * slot * 4 +
+           size_t(8 * nb) * (max_span * kSpanCols + 32) * 2;
+}
+
+
+// mode: 0 LUT part, 1 CSR part, 2 fused
+cudaError_t launch_bstream(uint32_t bits, uint32_t nb, const BStreamDevPlan& pl, const uint32_t* idx,
+                           const uint32_t* lut, const uint32_t* row_ptr, const uint32_t* csr,
+                           uint32_t rows, uint32_t cols, uint32_t ns, uint32_t tiles4,
+                           const uint16_t* x, uint32_t x_stride, uint32_t B, void* y,
+                           uint32_t y_stride, bool y_f16, int mode, cudaStream_t st) {
+    const int with_dense = mode != 1, with_csr = mode != 0;
+    const uint16_t* xT = with_dense && with_csr ? pl.xT : nullptr;
+    if (with_dense) {
+        BStreamParams p{};
+        p.idx = idx;
+        p.lut = lut;
+        p.x = x;
+        p.part = pl.part;
+        p.xT = const_cast<uint16_t*>(xT);
+        p.wdesc = pl.wdesc;
+        p.seg_base = pl.seg_base;
+        p.phase_span = pl.phase_span;
+        p.cols = cols;
+        p.ns = ns;
+        p.tiles4 = tiles4;
+        p.tiles16 = pl.tiles16;
+        p.B = B;
+        p.x_stride = x_stride;
+        p.xs_stride = pl.max_span * kSpanCols + 32;  // 32 mod 64 halves: conflict-free LDS.128
+        p.cs = pl.cs;
+        const uint32_t UW = bits * 32u, LW = bits == 3 ? 4u : 8u;
+        p.pw = pl.cs * UW + 16u;
+        p.lut_off = p.pw + pl.cs * UW;
+        p.pair = p.lut_off + 16u * LW;
+        p.slot_words = p.pair + p.pw + pl.cs * UW;
+        const size_t smem = bstream_smem_bytes(bits, nb, pl.max_span, pl.cs);
+        using K = void (*)(BStreamParams);
+        K k = bits == 3 ? (nb == 2 ? bstream_gemv<3, 2> : bstream_gemv<3, 1>)
+                        : (nb == 2 ? bstream_gemv<4, 2> : bstream_gemv<4, 1>);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        if ((e = launch_pdl_bs(k, dim3(pl.grid), dim3(kBsWarps * 32), smem, st, p)) != cudaSuccess)
+            return e;
+    }
+    const dim3 fg((rows + 7) / 8), fb(256);  // one warp per row
+    return nb == 2 ? launch_pdl_bs(bstream_finish<16>, fg, fb, 0, st, pl.part, pl.seg_base, pl.phases,
+                                   pl.tiles16, rows, B, row_ptr, csr, x, x_stride, xT, y, y_stride,
+                                   y_f16 ? 1 : 0, with_dense, with_csr)
+                   : launch_pdl_bs(bstream_finish<8>, fg, fb, 0, st, pl.part, pl.seg_base, pl.phases,
+                                   pl.tiles16, rows, B, row_ptr, csr, x, x_stride, xT, y, y_stride,
+                                   y_f16 ? 1 : 0, with_dense, with_csr);
+}
+
+}  // namespace sqz

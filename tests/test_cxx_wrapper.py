@@ -25,3 +25,16 @@ def test_cxx_wrapper_against_reference():
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=120)
     print(r.stdout, r.stderr)
     assert r.returncode == 0 and "PASS" in r.stdout
+
+
+PLAN_BIN = Path(__file__).resolve().parent / "cpp" / "test_bstream_plan"
+
+
+def test_bstream_plan_host_check():
+    """K11's work plan (csrc/bstream.cu): every cell decoded once, every
+    segment written once inside the range bstream_finish sums (no GPU)."""
+    if not PLAN_BIN.exists():
+        pytest.skip("make plan-test")
+    r = subprocess.run([str(PLAN_BIN)], capture_output=True, text=True, timeout=120)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "PASS" in r.stdout
