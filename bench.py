@@ -653,8 +653,9 @@ def model_stacks_bench(dev, peak: float, models=("13b", "65b"), tokens: int = 2)
 
 def batch_sweep_bench(dev, peak: float, reps: int = 50) -> list:
     """BASELINE configs[4] (a bounded slice): LLaMA-7B shapes, 3-bit + 0.45%,
-    batch 1/2/4/8/16, one fused product launch per batch (K7 with 2..8 vectors
-    sharing each decoded fragment, K8 beyond); bytes = weights once + the B
+    batch 1/2/4/8/16, one fused product per batch (K7 with 2..4 vectors
+    sharing each decoded fragment, K11 + its finish kernel beyond); bytes =
+    weights once + the B
     x / y vectors; layers rotate over > 256 MB."""
     import torch
     import paper_2306_07629_b200._native as N

@@ -413,6 +413,7 @@ struct dsq_cuda_layer {
     float* batch_part = nullptr;            // batched-product slice partials (lazy)
     BStreamDevPlan bs[2] = {};              // K9 plans for B <= 8 / <= 16 (lazy)
     void* bs_mem[2] = {nullptr, nullptr};   // their device allocations
+    bool bs_unsupported[2] = {false, false};  // too many column phases: K8
     uint32_t batch_kslices = 0, batch_spans = 0;
     std::mutex mu;       // guards dense_w materialization and batch_part
     std::mutex host_mu;  // serializes the host-buffer API on the internal stream
@@ -956,17 +957,21 @@ static BatchRoute batch_route(const dsq_cuda_layer* L, uint32_t batch) {
 // segment partials and the transposed x (caller holds L->mu)
 static int ensure_bstream(dsq_cuda_layer* L, uint32_t nb) {
     if (L->bs_mem[nb - 1]) return DSQ_OK;
-    const BStreamPlanHost h = bstream_plan(L->tiles, L->ns, L->bits, nb, uint32_t(L->num_sms));
-    const size_t smem = bstream_smem_bytes(L->bits, nb, h.max_span, h.cs);
-    if (smem > 232448 || h.phases > 255)
+    static const uint32_t warps = [] {
+        const char* e = std::getenv("DSQ_BS_WARPS");
+        return e && std::atoi(e) == 16 ? 16u : 8u;
+    }();
+    const BStreamPlanHost h = bstream_plan(L->tiles, L->ns, L->bits, nb, uint32_t(L->num_sms), warps);
+    const size_t smem = bstream_smem_bytes(L->bits, nb, h.max_span, h.cs, h.warps);
+    if (smem > 232448 || h.phases > kBsMaxPhases)
         return fail(DSQ_E_UNSUPPORTED, "batched plan: %zu bytes of shared memory, %u phases", smem,
                     h.phases);
     auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t b_w = up(h.wdesc.size() * 4), b_s = up(h.seg_base.size() * 4),
-                 b_p = up(h.phase_span.size() * 4), b_part = up(size_t(h.nseg) * 16 * 8 * nb * 4),
+                 b_part = up(size_t(h.nseg) * 16 * 8 * nb * 4),
                  b_xt = up(size_t(L->ns) * kSpanCols * 8 * nb * 2);
     uint8_t* m = nullptr;
-    CUDA_TRY(cudaMalloc(&m, b_w + b_s + b_p + b_part + b_xt));
+    CUDA_TRY(cudaMalloc(&m, b_w + b_s + b_part + b_xt));
     BStreamDevPlan& d = L->bs[nb - 1];
     d.phases = h.phases;
     d.nseg = h.nseg;
@@ -974,17 +979,18 @@ static int ensure_bstream(dsq_cuda_layer* L, uint32_t nb) {
     d.cs = h.cs;
     d.grid = h.grid;
     d.tiles16 = (L->tiles + 3) / 4;
+    d.warps = h.warps;
+    for (uint32_t k = 0; k <= h.phases; ++k) {
+        d.phase_span_h[k] = h.phase_span[k];
+        d.cta_pre_h[k] = h.cta_pre[k];
+    }
     d.wdesc = reinterpret_cast<uint4*>(m);
     d.seg_base = reinterpret_cast<uint32_t*>(m + b_w);
-    d.phase_span = reinterpret_cast<uint32_t*>(m + b_w + b_s);
-    d.part = reinterpret_cast<float*>(m + b_w + b_s + b_p);
-    d.xT = reinterpret_cast<uint16_t*>(m + b_w + b_s + b_p + b_part);
+    d.part = reinterpret_cast<float*>(m + b_w + b_s);
+    d.xT = reinterpret_cast<uint16_t*>(m + b_w + b_s + b_part);
     cudaError_t e = cudaMemcpy(d.wdesc, h.wdesc.data(), h.wdesc.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(d.seg_base, h.seg_base.data(), h.seg_base.size() * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(d.phase_span, h.phase_span.data(), h.phase_span.size() * 4,
-                       cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(m);
         return cuda_fail(e, "batched plan upload");
@@ -1008,13 +1014,23 @@ static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype,
     if (y_dtype != DSQ_F32 && y_dtype != DSQ_F16)
         return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
     const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
-    if (batch_route(L, batch) != BatchRoute::k8) {
-        const uint32_t nb = batch > 8 ? 2u : 1u;
-        {
-            std::lock_guard<std::mutex> lk(L->mu);
+    const uint32_t nb = batch > 8 ? 2u : 1u;
+    bool k11 = batch_route(L, batch) != BatchRoute::k8;
+    if (k11) {
+        std::lock_guard<std::mutex> lk(L->mu);
+        if (L->bs_unsupported[nb - 1]) {
+            k11 = false;
+        } else {
             const int rc = ensure_bstream(L, nb);
-            if (rc) return rc;
+            if (rc == DSQ_E_UNSUPPORTED) {  // more column phases than the launch carries: K8
+                L->bs_unsupported[nb - 1] = true;
+                k11 = false;
+            } else if (rc) {
+                return rc;
+            }
         }
+    }
+    if (k11) {
         CUDA_TRY(launch_bstream(L->bits, nb, L->bs[nb - 1], L->rec, L->tlut, L->P.row_ptr, L->P.csr,
                                 L->rows, L->cols, L->ns, L->tiles, static_cast<const uint16_t*>(x),
                                 x_stride, batch, y, y_stride, y_dtype == DSQ_F16, mode, st));
@@ -1506,6 +1522,11 @@ struct dsq_cuda_stack {
     bool seq = false;
     uint32_t batch = 1, y_dtype = DSQ_F16, launches = 1;
     std::vector<StackSeqStep> steps;
+    // the sequential form's launches captured once (after one eager run has
+    // created the layers' batched plans) and replayed as one graph launch
+    cudaStream_t seq_capture = nullptr;
+    cudaGraphExec_t seq_graph = nullptr;
+    uint32_t seq_runs = 0;
     // serving loop (dsq_cuda_serve_*): device [gate n][notify n][flag][err],
     // pinned host [host_done][doorbell] and the x staging buffer
     uint32_t* serve_dev = nullptr;
@@ -1843,15 +1864,45 @@ int dsq_cuda_stack_run(dsq_cuda_stack* S, void* stream) {
     if (S->serve_dev) return fail(DSQ_E_INVALID_ARGUMENT, "served stack: use dsq_cuda_serve_*");
     cudaSetDevice(S->device);
     if (S->seq) {
-        uint32_t launches = 0;
-        for (const StackSeqStep& q : S->steps) {
-            const int rc = gemv_impl(q.layer, DSQ_KERNEL_FUSED, q.x, DSQ_F16, q.y, int(S->y_dtype),
-                                     S->batch, static_cast<cudaStream_t>(stream), true,
-                                     q.x_stride, q.y_stride);
-            if (rc) return rc;
-            launches += S->batch == 1 || batch_route(q.layer, S->batch) == BatchRoute::k7 ? 1u : 2u;
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        auto enqueue = [&](cudaStream_t s) -> int {
+            uint32_t launches = 0;
+            for (const StackSeqStep& q : S->steps) {
+                const int rc = gemv_impl(q.layer, DSQ_KERNEL_FUSED, q.x, DSQ_F16, q.y,
+                                         int(S->y_dtype), S->batch, s, true, q.x_stride, q.y_stride);
+                if (rc) return rc;
+                launches += S->batch == 1 || batch_route(q.layer, S->batch) == BatchRoute::k7 ? 1u : 2u;
+            }
+            S->launches = launches;
+            return DSQ_OK;
+        };
+        if (S->seq_graph) {
+            CUDA_TRY(cudaGraphLaunch(S->seq_graph, st));
+            return DSQ_OK;
         }
-        S->launches = launches;
+        // first run: eager (creates the layers' batched plans and scratch),
+        // then capture the same launches on an internal stream while the GPU
+        // executes them; later runs are one graph launch, so the host never
+        // paces the ~2 launches per layer
+        const int rc0 = enqueue(st);
+        if (rc0 || S->seq_runs++ > 0) return rc0;
+        if (!S->seq_capture)
+            CUDA_TRY(cudaStreamCreateWithFlags(&S->seq_capture, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamBeginCapture(S->seq_capture, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue(S->seq_capture);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(S->seq_capture, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "sequential stack capture");
+        const cudaError_t e2 = cudaGraphInstantiate(&S->seq_graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e2 != cudaSuccess) {
+            S->seq_graph = nullptr;
+            return cuda_fail(e2, "sequential stack graph");
+        }
         return DSQ_OK;
     }
     if (S->tp) {
@@ -2054,6 +2105,8 @@ int dsq_cuda_stack_destroy(dsq_cuda_stack* S) {
     if (S->serve_dev) cudaFree(S->serve_dev);
     if (S->arena) cudaFree(S->arena);
     if (S->trace) cudaFree(S->trace);
+    if (S->seq_graph) cudaGraphExecDestroy(S->seq_graph);
+    if (S->seq_capture) cudaStreamDestroy(S->seq_capture);
     delete S;
     return DSQ_OK;
 }

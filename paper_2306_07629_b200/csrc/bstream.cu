@@ -41,9 +41,8 @@
 
 namespace sqz {
 
-constexpr int kBsWarps = 8;
-constexpr int kBsSlots = 3;
-constexpr uint32_t kBsBarBytes = 256;  // mbarrier area at the start of shared memory
+constexpr uint32_t kBsBarBytes = 512;  // mbarrier area at the start of shared memory
+__host__ __device__ constexpr uint32_t bs_slots(uint32_t warps) { return warps == 16 ? 2u : 3u; }
 
 struct BStreamParams {
     const uint32_t* idx;         // [tiles4][ns][UW]
@@ -53,7 +52,9 @@ struct BStreamParams {
     uint16_t* xT;                // [ns*256][8*NB] x transposed for the CSR pass (or null)
     const uint4* wdesc;          // [grid*8] {cell_begin, cell_end, seg_first, bs_pack_w(phase, a, gp)}
     const uint32_t* seg_base;    // [phases*tiles16 + 1]
-    const uint32_t* phase_span;  // [phases + 1] span boundaries
+    uint32_t phases;
+    uint32_t phase_span[kBsMaxPhases + 1];  // span boundaries of the phases
+    uint32_t cta_pre[kBsMaxPhases + 1];     // CTAs of phase k: cta_pre[k] .. cta_pre[k+1]
     uint32_t cols, ns, tiles4, tiles16, B, x_stride;
     uint32_t xs_stride;    // halves per staged x row (max phase spans * 256 + 32)
     uint32_t cs;           // spans per chunk
@@ -147,8 +148,11 @@ __device__ __forceinline__ void bs_cell(const uint32_t* u0, const uint32_t* u1, 
     }
 }
 
-template <int BITS, int NB>  // NB = HMMA column groups (1: B <= 8, 2: B <= 16)
-__global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_constant__ BStreamParams p) {
+// NB = HMMA column groups (1: B <= 8, 2: B <= 16); W = decode warps per CTA
+template <int BITS, int NB, int W>
+__global__ void __launch_bounds__(W * 32, 1) bstream_gemv(const __grid_constant__ BStreamParams p) {
+    constexpr int kBsWarps = W;
+    constexpr int kBsSlots = int(bs_slots(W));
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t LW = BITS == 3 ? 4u : 8u;
     constexpr uint32_t UW = BITS * 32u;
@@ -158,10 +162,14 @@ __global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_co
     uint32_t* ring = reinterpret_cast<uint32_t*>(smem + kBsBarBytes) + warp * kBsSlots * p.slot_words;
     uint16_t* xs = reinterpret_cast<uint16_t*>(reinterpret_cast<uint32_t*>(smem + kBsBarBytes) +
                                                kBsWarps * kBsSlots * p.slot_words);
-    const uint4 wd = p.wdesc[blockIdx.x * kBsWarps + warp];
-    const uint32_t phase = wd.w & 0xffu;
+    // the warp's cell range from the launch parameters (no dependent load
+    // before the first weight copies); its first segment id arrives by the
+    // time the range first leaves a tile
+    uint32_t phase, cta_a, cta_gp, cb, ce;
+    bs_warp_range(p.phase_span, p.cta_pre, p.phases, p.tiles16, blockIdx.x, warp, W, &phase,
+                  &cta_a, &cta_gp, &cb, &ce);
     const uint32_t sa = p.phase_span[phase], S = p.phase_span[phase + 1] - sa;
-    const uint32_t cb = wd.x, ce = wd.y;
+    const uint32_t seg_first = p.wdesc[blockIdx.x * kBsWarps + warp].z;
     // chunk at cell c: 16-row tile q = c / S, phase-local span c % S, up to cs
     // spans, not past the tile's last span or the warp's range
     auto issue = [&](uint32_t c, uint32_t slot, uint64_t pol) -> uint32_t {
@@ -219,9 +227,8 @@ __global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_co
         if (p.xT) {
             // this CTA's share of the phase's transposed x: all vectors of a
             // column in one 16- / 32-byte run for the CSR gathers
-            const uint32_t a = (wd.w >> 8) & 0xfffu, gp = wd.w >> 20;
-            const uint32_t x0 = uint32_t(uint64_t(ccount) * a / gp);
-            const uint32_t x1 = uint32_t(uint64_t(ccount) * (a + 1) / gp);
+            const uint32_t x0 = uint32_t(uint64_t(ccount) * cta_a / cta_gp);
+            const uint32_t x1 = uint32_t(uint64_t(ccount) * (cta_a + 1) / cta_gp);
             for (uint32_t k = x0 * NB + threadIdx.x; k < x1 * NB; k += blockDim.x) {
                 const uint32_t c = k / NB, j = k - c * NB;
                 uint32_t h[4];
@@ -238,12 +245,16 @@ __global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_co
     const uint32_t g = lane >> 2, t = lane & 3, i = g & 3, j0 = g >> 2;  // rows g, g+8: tiles j0, j0+2
     const uint16_t* xg0 = xs + g * p.xs_stride;        // vector g
     const uint16_t* xg1 = xs + (8 + g) * p.xs_stride;  // vector 8 + g (NB == 2)
-    float d[2][NB][4];
+    // two accumulator sets (even / odd span of the unrolled pair), each with
+    // one chain per h: 4 * NB independent HMMA chains
+    float d[2][NB][4], e[2][NB][4];
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int n = 0; n < NB; ++n) d[c][n][0] = d[c][n][1] = d[c][n][2] = d[c][n][3] = 0.f;
-    uint32_t seg = wd.z;
+        for (int n = 0; n < NB; ++n)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) d[c][n][r] = e[c][n][r] = 0.f;
+    uint32_t seg = seg_first;
     uint32_t it = 0;
     for (uint32_t c = cb; c < ce;) {
         const uint32_t q = c / S, sl = c - q * S;
@@ -271,7 +282,11 @@ __global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_co
         uint32_t u = 0;
         for (; u + 2 <= n; u += 2, u0 += 2 * UW, u1 += 2 * UW) {  // two spans: independent chains
             bs_cell<BITS, NB>(u0, u1, (sl + u) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
-            bs_cell<BITS, NB>(u0 + UW, u1 + UW, (sl + u + 1) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
+            // 16 warps: one accumulator set (the registers of 512 threads)
+            if constexpr (W == 16)
+                bs_cell<BITS, NB>(u0 + UW, u1 + UW, (sl + u + 1) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
+            else
+                bs_cell<BITS, NB>(u0 + UW, u1 + UW, (sl + u + 1) * kSpanCols, i, t, P0, P1, xg0, xg1, e);
         }
         if (u < n) bs_cell<BITS, NB>(u0, u1, (sl + u) * kSpanCols, i, t, P0, P1, xg0, xg1, d);
         // the slot's words are in registers or consumed: refill it
@@ -286,11 +301,15 @@ __global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_co
             for (int nn = 0; nn < NB; ++nn) {
                 const uint32_t b0 = 8 * nn + 2 * t;
                 *reinterpret_cast<float2*>(out + g * NBV + b0) =
-                    make_float2(d[0][nn][0] + d[1][nn][0], d[0][nn][1] + d[1][nn][1]);
+                    make_float2((d[0][nn][0] + d[1][nn][0]) + (e[0][nn][0] + e[1][nn][0]),
+                                (d[0][nn][1] + d[1][nn][1]) + (e[0][nn][1] + e[1][nn][1]));
                 *reinterpret_cast<float2*>(out + (g + 8) * NBV + b0) =
-                    make_float2(d[0][nn][2] + d[1][nn][2], d[0][nn][3] + d[1][nn][3]);
+                    make_float2((d[0][nn][2] + d[1][nn][2]) + (e[0][nn][2] + e[1][nn][2]),
+                                (d[0][nn][3] + d[1][nn][3]) + (e[0][nn][3] + e[1][nn][3]));
 #pragma unroll
-                for (int cc = 0; cc < 2; ++cc) d[cc][nn][0] = d[cc][nn][1] = d[cc][nn][2] = d[cc][nn][3] = 0.f;
+                for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) d[cc][nn][r] = e[cc][nn][r] = 0.f;
             }
             // a later tile of this range starts with this warp: its first segment
             if (c < ce) seg = p.seg_base[phase * p.tiles16 + q + 1];
@@ -298,12 +317,16 @@ __global__ void __launch_bounds__(kBsWarps * 32, 1) bstream_gemv(const __grid_co
     }
 }
 
-// y[b][r] = sum of the row's segments (phase by phase, in segment order) +
-// its CSR deltas.  One warp per row: lane = part * XB + b (XB = 8 * NB), the
-// CSR entries split over the 32 / XB parts in groups of 8 and added in a fixed
-// shuffle order, as batch_finish (batch.cu).
+// y[b][r] = the row's segments + its CSR deltas.  One warp per row: lane =
+// part * XB + b (XB = 8 * NB, P = 32 / XB parts).  Part k sums every P-th
+// segment of each phase and every P-th group of 8 CSR entries; the parts are
+// then added in a fixed shuffle order (deterministic).  All loads that do not
+// depend on each other are issued together: the row pointers and the
+// phases' segment bounds in one round trip, then the segments and the CSR
+// entries, then the transposed x (as batch_finish in batch.cu, but ~3 dependent
+// round trips per row instead of ~5).
 template <int XB>
-__global__ void bstream_finish(const float* __restrict__ part, const uint32_t* __restrict__ seg_base,
+__global__ void __launch_bounds__(256) bstream_finish(const float* __restrict__ part, const uint32_t* __restrict__ seg_base,
                                uint32_t phases, uint32_t tiles16, uint32_t rows, uint32_t B,
                                const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
                                const uint16_t* __restrict__ x, uint32_t x_stride,
@@ -315,37 +338,49 @@ __global__ void bstream_finish(const float* __restrict__ part, const uint32_t* _
     const uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const uint32_t lane = threadIdx.x & 31, b = lane % XB, k = lane / XB;
     if (r >= rows) return;  // whole warps
-    const bool live = b < B;
+    const uint32_t q16 = r >> 4, rr = r & 15u;
+    uint32_t sb = 0, rp = 0;
+    if (with_dense && lane < 2 * phases) sb = seg_base[(lane >> 1) * tiles16 + q16 + (lane & 1)];
+    if (with_csr && lane >= 30) rp = row_ptr[r + (lane - 30)];
     float s = 0.f;
-    if (with_csr && live) {
-        const uint16_t* xb = xT ? xT + b : x + size_t(b) * x_stride;
-        const uint32_t xs = xT ? uint32_t(XB) : 1u;
-        const uint32_t q0 = row_ptr[r], q1 = row_ptr[r + 1];
-        for (uint32_t q = q0 + 8 * k; q < q1; q += 8 * P) {
-            uint32_t e[8];
+    if (with_dense) {
+        for (uint32_t ph = 0; ph < phases; ++ph) {
+            uint32_t s0, s1;
+            if (phases <= 16) {
+                s0 = __shfl_sync(0xffffffffu, sb, 2 * ph);
+                s1 = __shfl_sync(0xffffffffu, sb, 2 * ph + 1);
+            } else {
+                s0 = seg_base[ph * tiles16 + q16];
+                s1 = seg_base[ph * tiles16 + q16 + 1];
+            }
+#pragma unroll 4
+            for (uint32_t sg = s0 + k; sg < s1; sg += P) s += __ldcg(part + (size_t(sg) * 16 + rr) * XB + b);
+        }
+    }
+    if (with_csr) {
+        const uint32_t q0 = __shfl_sync(0xffffffffu, rp, 30), q1 = __shfl_sync(0xffffffffu, rp, 31);
+        if (b < B) {
+            const uint16_t* xb = xT ? xT + b : x + size_t(b) * x_stride;
+            const uint32_t xs = xT ? uint32_t(XB) : 1u;
+            float c = 0.f;
+            for (uint32_t q = q0 + 8 * k; q < q1; q += 8 * P) {
+                uint32_t e[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) e[u] = q + u < q1 ? __ldg(csr + q + u) : 0u;
-            uint16_t xv[8];
+                for (int u = 0; u < 8; ++u) e[u] = q + u < q1 ? __ldg(csr + q + u) : 0u;
+                uint16_t xv[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                xv[u] = q + u < q1 ? __ldg(xb + size_t(e[u] & 0xffffu) * xs) : uint16_t(0);
+                for (int u = 0; u < 8; ++u)
+                    xv[u] = q + u < q1 ? ld_cg_u16(xb + size_t(e[u] & 0xffffu) * xs) : uint16_t(0);
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (q + u < q1) s = fma_h(uint16_t(e[u] >> 16), xv[u], s);
+                for (int u = 0; u < 8; ++u)
+                    if (q + u < q1) c = fma_h(uint16_t(e[u] >> 16), xv[u], c);
+            }
+            s += c;
         }
     }
 #pragma unroll
     for (uint32_t o = XB; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (k != 0 || !live) return;
-    if (with_dense) {
-        const uint32_t q = r >> 4, rr = r & 15u;
-        float dsum = 0.f;
-        for (uint32_t ph = 0; ph < phases; ++ph) {
-            const uint32_t s0 = seg_base[ph * tiles16 + q], s1 = seg_base[ph * tiles16 + q + 1];
-            for (uint32_t sg = s0; sg < s1; ++sg) dsum += part[(size_t(sg) * 16 + rr) * XB + b];
-        }
-        s = dsum + s;
-    }
+    if (k != 0 || b >= B) return;
     if (y_f16)
         static_cast<__half*>(y)[size_t(b) * y_stride + r] = __float2half_rn(s);
     else
@@ -374,8 +409,10 @@ static cudaError_t launch_pdl_bs(K kern, dim3 grid, dim3 block, size_t smem, cud
 // Split a layer (tiles4 4-row tiles, ns spans) for B <= 8 * nb vectors over
 // `grid` CTAs.  Pure host arithmetic (unit-tested through the C ABI).
 BStreamPlanHost bstream_plan(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32_t nb,
-                             uint32_t grid) {
+                             uint32_t grid, uint32_t warps) {
     BStreamPlanHost pl;
+    const uint32_t kBsWarps = warps == 16 ? 16u : 8u;
+    pl.warps = kBsWarps;
     const uint32_t T = (tiles4 + 3) / 4;
     const uint32_t smax = nb == 2 ? 8u : 16u;  // 64 KB of staged x per phase
     const uint32_t P = std::max<uint32_t>(1, (ns + smax - 1) / smax);  // <= 255 (wdesc .w)
@@ -384,7 +421,7 @@ BStreamPlanHost bstream_plan(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32
     for (uint32_t k = 0; k <= P; ++k) pl.phase_span[k] = uint32_t(uint64_t(k) * ns / P);
     for (uint32_t k = 0; k < P; ++k)
         pl.max_span = std::max(pl.max_span, pl.phase_span[k + 1] - pl.phase_span[k]);
-    pl.cs = bits == 3 ? 4u : 3u;
+    pl.cs = kBsWarps == 16 ? 2u : bits == 3 ? 4u : 3u;
     grid = std::max(grid, P);
     pl.grid = grid;
     // CTAs per phase in proportion to the phase's spans (>= 1 each)
@@ -397,27 +434,25 @@ BStreamPlanHost bstream_plan(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32
     }
     // floor(grid * sp / ns) >= 1 for balanced phases, so used <= grid here
     for (uint32_t k = 0; used < grid; k = (k + 1) % P, ++used) ++gp[k];
-    // warp ranges, then segment counts per (phase, tile16)
+    pl.cta_pre.assign(P + 1, 0);
+    for (uint32_t k = 0; k < P; ++k) pl.cta_pre[k + 1] = pl.cta_pre[k] + gp[k];
+    // warp ranges (bs_warp_range: the kernel's own arithmetic), then segment
+    // counts per (phase, tile16)
     pl.wdesc.assign(size_t(grid) * kBsWarps * 4, 0);
     std::vector<uint32_t> pieces(size_t(P) * T, 0);
-    uint32_t cta = 0;
-    for (uint32_t k = 0; k < P; ++k) {
-        const uint32_t S = pl.phase_span[k + 1] - pl.phase_span[k];
-        const uint64_t C = uint64_t(T) * S;
-        for (uint32_t a = 0; a < gp[k]; ++a, ++cta) {
-            const uint64_t cb = C * a / gp[k], ce = C * (a + 1) / gp[k];
-            for (uint32_t w = 0; w < uint32_t(kBsWarps); ++w) {
-                const uint32_t wb = uint32_t(cb + (ce - cb) * w / kBsWarps);
-                const uint32_t we = uint32_t(cb + (ce - cb) * (w + 1) / kBsWarps);
-                uint32_t* d = &pl.wdesc[(size_t(cta) * kBsWarps + w) * 4];
-                d[0] = wb;
-                d[1] = we;
-                d[3] = bs_pack_w(k, a, gp[k]);
-                if (wb < we)
-                    for (uint32_t q = wb / S; q <= (we - 1) / S; ++q) ++pieces[size_t(k) * T + q];
-            }
+    for (uint32_t cta = 0; cta < grid; ++cta)
+        for (uint32_t w = 0; w < uint32_t(kBsWarps); ++w) {
+            uint32_t k, a, g, wb, we;
+            bs_warp_range(pl.phase_span.data(), pl.cta_pre.data(), P, T, cta, w, kBsWarps, &k, &a, &g,
+                          &wb, &we);
+            const uint32_t S = pl.phase_span[k + 1] - pl.phase_span[k];
+            uint32_t* d = &pl.wdesc[(size_t(cta) * kBsWarps + w) * 4];
+            d[0] = wb;
+            d[1] = we;
+            d[3] = bs_pack_w(k, a, g);
+            if (wb < we)
+                for (uint32_t q = wb / S; q <= (we - 1) / S; ++q) ++pieces[size_t(k) * T + q];
         }
-    }
     pl.seg_base.assign(size_t(P) * T + 1, 0);
     for (size_t z = 0; z < size_t(P) * T; ++z) pl.seg_base[z + 1] = pl.seg_base[z] + pieces[z];
     pl.nseg = pl.seg_base[size_t(P) * T];
@@ -436,7 +471,9 @@ BStreamPlanHost bstream_plan(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32
     return pl;
 }
 
-size_t bstream_smem_bytes(uint32_t bits, uint32_t nb, uint32_t max_span, uint32_t cs) {
+size_t bstream_smem_bytes(uint32_t bits, uint32_t nb, uint32_t max_span, uint32_t cs,
+                          uint32_t warps) {
+    const uint32_t kBsWarps = warps, kBsSlots = bs_slots(warps);
     const uint32_t LW = bits == 3 ? 4u : 8u, UW = bits * 32u;
     const size_t slot = 2u * (cs * UW + 16u) + 2u * cs * UW + 16u * LW;  // BStreamParams
     return kBsBarBytes + size_t(kBsWarps) * kBsSlots * slot * 4 +
@@ -461,7 +498,11 @@ cudaError_t launch_bstream(uint32_t bits, uint32_t nb, const BStreamDevPlan& pl,
         p.xT = const_cast<uint16_t*>(xT);
         p.wdesc = pl.wdesc;
         p.seg_base = pl.seg_base;
-        p.phase_span = pl.phase_span;
+        p.phases = pl.phases;
+        for (uint32_t k = 0; k <= pl.phases; ++k) {
+            p.phase_span[k] = pl.phase_span_h[k];
+            p.cta_pre[k] = pl.cta_pre_h[k];
+        }
         p.cols = cols;
         p.ns = ns;
         p.tiles4 = tiles4;
@@ -475,22 +516,38 @@ cudaError_t launch_bstream(uint32_t bits, uint32_t nb, const BStreamDevPlan& pl,
         p.lut_off = p.pw + pl.cs * UW;
         p.pair = p.lut_off + 16u * LW;
         p.slot_words = p.pair + p.pw + pl.cs * UW;
-        const size_t smem = bstream_smem_bytes(bits, nb, pl.max_span, pl.cs);
+        const size_t smem = bstream_smem_bytes(bits, nb, pl.max_span, pl.cs, pl.warps);
         using K = void (*)(BStreamParams);
-        K k = bits == 3 ? (nb == 2 ? bstream_gemv<3, 2> : bstream_gemv<3, 1>)
-                        : (nb == 2 ? bstream_gemv<4, 2> : bstream_gemv<4, 1>);
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        if ((e = launch_pdl_bs(k, dim3(pl.grid), dim3(kBsWarps * 32), smem, st, p)) != cudaSuccess)
+        static const K kerns[8] = {bstream_gemv<3, 1, 8>,  bstream_gemv<3, 2, 8>,
+                                   bstream_gemv<4, 1, 8>,  bstream_gemv<4, 2, 8>,
+                                   bstream_gemv<3, 1, 16>, bstream_gemv<3, 2, 16>,
+                                   bstream_gemv<4, 1, 16>, bstream_gemv<4, 2, 16>};
+        const int ki = (pl.warps == 16 ? 4 : 0) + (bits == 3 ? 0 : 2) + (nb == 2 ? 1 : 0);
+        const K k = kerns[ki];
+        // the shared-memory opt-in once per kernel and device (the attribute
+        // call costs microseconds of host time per product otherwise)
+        static bool attr_done[8][64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaError_t e = cudaSuccess;
+        if (dev < 0 || dev >= 64 || !attr_done[ki][dev]) {
+            int max_optin = 0;
+            cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            if (size_t(max_optin) < smem) return cudaErrorInvalidValue;
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+            if (e != cudaSuccess) return e;
+            if (dev >= 0 && dev < 64) attr_done[ki][dev] = true;
+        }
+        if ((e = launch_pdl_bs(k, dim3(pl.grid), dim3(pl.warps * 32), smem, st, p)) != cudaSuccess)
             return e;
     }
-    const dim3 fg((rows + 7) / 8), fb(256);  // one warp per row
-    return nb == 2 ? launch_pdl_bs(bstream_finish<16>, fg, fb, 0, st, pl.part, pl.seg_base, pl.phases,
-                                   pl.tiles16, rows, B, row_ptr, csr, x, x_stride, xT, y, y_stride,
-                                   y_f16 ? 1 : 0, with_dense, with_csr)
-                   : launch_pdl_bs(bstream_finish<8>, fg, fb, 0, st, pl.part, pl.seg_base, pl.phases,
-                                   pl.tiles16, rows, B, row_ptr, csr, x, x_stride, xT, y, y_stride,
-                                   y_f16 ? 1 : 0, with_dense, with_csr);
+    const dim3 fg((rows + 7) / 8);  // one warp per row
+    return nb == 2 ? launch_pdl_bs(bstream_finish<16>, fg, dim3(256), 0, st, pl.part, pl.seg_base,
+                                   pl.phases, pl.tiles16, rows, B, row_ptr, csr, x, x_stride, xT, y,
+                                   y_stride, y_f16 ? 1 : 0, with_dense, with_csr)
+                   : launch_pdl_bs(bstream_finish<8>, fg, dim3(256), 0, st, pl.part, pl.seg_base,
+                                   pl.phases, pl.tiles16, rows, B, row_ptr, csr, x, x_stride, xT, y,
+                                   y_stride, y_f16 ? 1 : 0, with_dense, with_csr);
 }
 
 }  // namespace sqz

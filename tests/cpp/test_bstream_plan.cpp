@@ -14,8 +14,10 @@
 
 using namespace sqz;
 
-static int check(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32_t nb, uint32_t grid) {
-    const BStreamPlanHost pl = bstream_plan(tiles4, ns, bits, nb, grid);
+static int check(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32_t nb, uint32_t grid,
+                 uint32_t warps) {
+    const BStreamPlanHost pl = bstream_plan(tiles4, ns, bits, nb, grid, warps);
+    const uint32_t W = pl.warps;
     const uint32_t T = (tiles4 + 3) / 4;
     std::vector<int> cover(size_t(T) * ns, 0), seguse(pl.nseg, 0), xt(pl.phases, 0);
     std::vector<uint32_t> xt_gp(pl.phases, 0);
@@ -24,8 +26,8 @@ static int check(uint32_t tiles4, uint32_t ns, uint32_t bits, uint32_t nb, uint3
         return 1;
     }
     for (uint32_t c = 0; c < pl.grid; ++c) {
-        for (uint32_t w = 0; w < 8; ++w) {
-            const uint32_t* d = &pl.wdesc[(size_t(c) * 8 + w) * 4];
+        for (uint32_t w = 0; w < W; ++w) {
+            const uint32_t* d = &pl.wdesc[(size_t(c) * W + w) * 4];
             const uint32_t ph = d[3] & 0xffu, a = (d[3] >> 8) & 0xfffu, gp = d[3] >> 20;
             if (ph >= pl.phases) return std::printf("FAIL phase %u\n", ph), 1;
             if (w == 0) {
@@ -70,7 +72,8 @@ int main() {
     for (const auto& s : shapes)
         for (uint32_t nb = 1; nb <= 2; ++nb)
             for (uint32_t bits = 3; bits <= 4; ++bits)
-                for (uint32_t grid : {148u, 132u, 1u}) bad |= check(s[0], s[1], bits, nb, grid), ++n;
+                for (uint32_t grid : {148u, 132u, 1u})
+                    for (uint32_t warps : {8u, 16u}) bad |= check(s[0], s[1], bits, nb, grid, warps), ++n;
     std::printf("%s (%d plans)\n", bad ? "FAIL" : "PASS", n);
     return bad;
 }

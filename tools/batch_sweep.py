@@ -2,10 +2,10 @@
 3- and 4-bit, sparsity 0 / 0.05% / 0.45%, fused Dense-and-Sparse products.
 
 Batch 1 runs the persistent tensor-core LUT-GEMV (K7, dsq_cuda_gemv batch=1);
-batch 2..8 the same kernel with 2/4/8 x vectors sharing every decoded fragment
-(when they fit in shared memory next to the ring), batch 9..16 (and the rest)
-the batched LUT-GEMM (K8, dense 16-row HMMA fragments, batch in the N
-dimension, decode amortised over the batch).  Each configuration rotates
+batch 2..4 the same kernel with 2/4 x vectors sharing every decoded fragment
+(when they fit in shared memory next to the ring), batch 5..16 (and the rest)
+the batched LUT-GEMM K11 (csrc/bstream.cu: dense 16-row HMMA fragments, batch
+in the N dimension, per-warp TMA rings, decode amortised over the batch).  Each configuration rotates
 over enough distinct device layers that the working set exceeds L2 and
 times back-to-back products with CUDA events.  Prints one JSON line per
 (shape, bits, sparsity, batch): µs per product, weight-stream GB/s
@@ -74,9 +74,9 @@ def main():
                     print(json.dumps({
                         "shape": shp, "bits": bits, "sparsity": sp, "batch": B,
                         "kernel": ("K7 persistent (batch 1)" if B == 1 else
-                                   f"K7 persistent NB={2 if B == 2 else 4 if B <= 4 else 8} "
-                                   "(K8 when the x vectors do not fit)" if B <= 8 else
-                                   "K8 batched HMMA"),
+                                   f"K7 persistent NB={2 if B == 2 else 4} "
+                                   "(K11 when the x vectors do not fit)" if B <= 4 else
+                                   "K11 batched HMMA (TMA rings) + finish"),
                         "us": round(us, 3), "GBs": round(bytes_b / us / 1e3, 1),
                         "TFLOPs": round(flops / us / 1e6, 2),
                         "speedup_vs_B_x_batch1": round(B * base_us / us, 2) if base_us else None,
