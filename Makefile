@@ -6,7 +6,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas 
 PKG       := paper_2306_07629_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libdsq_cuda.so
-OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/batch.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
+OBJS      := $(CSRC)/kernels.o $(CSRC)/stack.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 
 all: $(LIB) oracle cxx-test plan-test
 
@@ -15,9 +15,6 @@ $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/layout.hpp $(CSRC)/ptx.cuh
 
 $(CSRC)/stack.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/layout.hpp $(CSRC)/tile.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/stack.ptxas.log || (cat $(CSRC)/stack.ptxas.log; false)
-
-$(CSRC)/batch.o: $(CSRC)/batch.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/batch.ptxas.log || (cat $(CSRC)/batch.ptxas.log; false)
 
 $(CSRC)/bstream.o: $(CSRC)/bstream.cu $(CSRC)/bstream.hpp $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/bstream.ptxas.log || (cat $(CSRC)/bstream.ptxas.log; false)
@@ -53,7 +50,7 @@ PROFLIB := $(PKG)/libdsq_cuda_prof.so
 profile-lib: $(PROFLIB)
 $(CSRC)/stack_prof.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_PROFILE -c $< -o $@ 2> /dev/null
-$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/batch.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
+$(PROFLIB): $(CSRC)/kernels.o $(CSRC)/stack_prof.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 # debug variant: bounded waits that trap with the waiting site (stack.cu)
@@ -61,7 +58,7 @@ WDLIB := $(PKG)/libdsq_cuda_wd.so
 watchdog-lib: $(WDLIB)
 $(CSRC)/stack_wd.o: $(CSRC)/stack.cu $(CSRC)/stack.hpp $(CSRC)/ptx.cuh $(CSRC)/tile.cuh $(CSRC)/layout.hpp
 	$(NVCC) $(NVFLAGS) -DDSQ_STACK_WATCHDOG -c $< -o $@
-$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/batch.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
+$(WDLIB): $(CSRC)/kernels.o $(CSRC)/stack_wd.o $(CSRC)/bstream.o $(CSRC)/api.o $(CSRC)/container.o $(CSRC)/roofline.o $(CSRC)/quantize.o $(CSRC)/decompose.o $(CSRC)/quantize_api.o $(CSRC)/shard.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lgomp
 
 oracle:

@@ -38,12 +38,6 @@ cudaError_t launch_f32_to_f16(const float* in, uint16_t* out, uint32_t n, cudaSt
                               bool pdl);
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_upload_x(const void* host, void* dev, size_t bytes, cudaStream_t st);
-cudaError_t launch_batch(uint32_t bits, const uint32_t* idx, const uint32_t* lut,
-                         const uint32_t* row_ptr, const uint32_t* csr, uint32_t rows,
-                         uint32_t cols, uint32_t ns, uint32_t tiles4, const uint16_t* x,
-                         uint32_t x_stride, uint32_t B, void* y, uint32_t y_stride, bool y_f16,
-                         float* part, uint32_t kslices, uint32_t spans_per_slice, int mode,
-                         cudaStream_t st);
 cudaError_t launch_apply_deltas(const uint32_t* row_ptr, const uint32_t* csr, const uint16_t* lut,
                                 uint32_t K, uint32_t groups, uint32_t gcols, uint32_t rows,
                                 uint32_t cols, float* w, cudaStream_t st);
@@ -402,7 +396,7 @@ struct dsq_cuda_layer {
     float* gseg1 = nullptr;
     StackParams sp2{}, sp4{}, sp8{};        // batch 2 / 3..4 / 5..8 single-layer plans (lazy)
     bool sp2_ready = false, sp4_ready = false, sp8_ready = false;
-    bool sp2_failed = false, sp4_failed = false, sp8_failed = false;  // x does not fit: K8
+    bool sp2_failed = false, sp4_failed = false, sp8_failed = false;  // x does not fit: K11
     bool k7_batch_failed(uint32_t nb) const {
         return nb == 2 ? sp2_failed : nb == 4 ? sp4_failed : sp8_failed;
     }
@@ -410,12 +404,9 @@ struct dsq_cuda_layer {
     float* gseg4 = nullptr;
     float* gseg8 = nullptr;
     cudaStream_t stream = nullptr;
-    float* batch_part = nullptr;            // batched-product slice partials (lazy)
     BStreamDevPlan bs[2] = {};              // K9 plans for B <= 8 / <= 16 (lazy)
     void* bs_mem[2] = {nullptr, nullptr};   // their device allocations
-    bool bs_unsupported[2] = {false, false};  // too many column phases: K8
-    uint32_t batch_kslices = 0, batch_spans = 0;
-    std::mutex mu;       // guards dense_w materialization and batch_part
+    std::mutex mu;       // guards dense_w materialization and the batched plans
     std::mutex host_mu;  // serializes the host-buffer API on the internal stream
 };
 
@@ -894,7 +885,6 @@ int dsq_cuda_layer_destroy(dsq_cuda_layer* L) {
     if (L->x16_pin) cudaFreeHost(L->x16_pin);
     if (L->y32_pin) cudaFreeHost(L->y32_pin);
     if (L->dense_w) cudaFree(L->dense_w);
-    if (L->batch_part) cudaFree(L->batch_part);
     for (void* m : L->bs_mem)
         if (m) cudaFree(m);
     if (L->gseg2) cudaFree(L->gseg2);
@@ -938,19 +928,17 @@ static int ensure_dense(dsq_cuda_layer* L, cudaStream_t st) {
 // which kernel runs a batched product: K7 (the persistent batch-1 kernel with
 // NB = 2 / 4 / 8 vectors per decoded fragment) for batch 2..4, K11 (bstream.cu:
 // dense fragment map on per-warp TMA rings) for 5..16 and for batches whose x
-// does not fit next to K7's ring.  DSQ_BATCH_PATH=k7 / k8 selects K7 (up to
-// batch 8) or the older K8 (batch.cu) instead, for A/B measurements.
-enum class BatchRoute { k7, k8, k11 };
+// does not fit next to K7's ring.  DSQ_BATCH_PATH=k7 runs batch 5..8 on K7
+// (NB = 8) instead, for A/B measurements.
+enum class BatchRoute { k7, k11 };
 static BatchRoute batch_route(const dsq_cuda_layer* L, uint32_t batch) {
-    static const int forced = [] {
+    static const bool k7_to_8 = [] {
         const char* e = std::getenv("DSQ_BATCH_PATH");
-        return !e ? 0 : !std::strcmp(e, "k7") ? 7 : !std::strcmp(e, "k8") ? 8 : 0;
+        return e && !std::strcmp(e, "k7");
     }();
     const uint32_t nbk = batch == 2 ? 2u : batch <= 4 ? 4u : 8u;
-    if (forced == 8 && batch > 4) return BatchRoute::k8;
-    if ((batch <= 4 || (forced == 7 && batch <= 8)) && !L->k7_batch_failed(nbk))
-        return BatchRoute::k7;
-    return forced == 8 ? BatchRoute::k8 : BatchRoute::k11;
+    if ((batch <= 4 || (k7_to_8 && batch <= 8)) && !L->k7_batch_failed(nbk)) return BatchRoute::k7;
+    return BatchRoute::k11;
 }
 
 // K11's plan for B <= 8 * nb vectors: warp ranges, segment numbering, the
@@ -999,7 +987,7 @@ static int ensure_bstream(dsq_cuda_layer* L, uint32_t nb) {
     return DSQ_OK;
 }
 
-// batched products on K11 (bstream.cu) or K8 (batch.cu): x [batch][cols]
+// batched products on K11 (bstream.cu): x [batch][cols]
 // fp16, y [batch][rows]
 static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype, void* y,
                       int y_dtype, uint32_t batch, cudaStream_t st, uint32_t x_stride,
@@ -1015,47 +1003,14 @@ static int gemv_batch(dsq_cuda_layer* L, int kernel, const void* x, int x_dtype,
         return fail(DSQ_E_INVALID_ARGUMENT, "y dtype must be F32 or F16");
     const int mode = kernel == DSQ_KERNEL_LUT ? 0 : kernel == DSQ_KERNEL_CSR ? 1 : 2;
     const uint32_t nb = batch > 8 ? 2u : 1u;
-    bool k11 = batch_route(L, batch) != BatchRoute::k8;
-    if (k11) {
-        std::lock_guard<std::mutex> lk(L->mu);
-        if (L->bs_unsupported[nb - 1]) {
-            k11 = false;
-        } else {
-            const int rc = ensure_bstream(L, nb);
-            if (rc == DSQ_E_UNSUPPORTED) {  // more column phases than the launch carries: K8
-                L->bs_unsupported[nb - 1] = true;
-                k11 = false;
-            } else if (rc) {
-                return rc;
-            }
-        }
-    }
-    if (k11) {
-        CUDA_TRY(launch_bstream(L->bits, nb, L->bs[nb - 1], L->rec, L->tlut, L->P.row_ptr, L->P.csr,
-                                L->rows, L->cols, L->ns, L->tiles, static_cast<const uint16_t*>(x),
-                                x_stride, batch, y, y_stride, y_dtype == DSQ_F16, mode, st));
-        return DSQ_OK;
-    }
     {
         std::lock_guard<std::mutex> lk(L->mu);
-        if (!L->batch_part) {
-            // column slices so that (row groups of 128) x slices >= 4 CTAs per SM
-            // (latency hiding for the index-word loads), at most 2 spans each
-            const uint32_t tiles16 = (L->tiles + 3) / 4, groups = (tiles16 + 7) / 8;
-            const uint32_t want = std::max<uint32_t>(1, ceil_div(4u * uint32_t(L->num_sms), groups));
-            L->batch_spans = std::max<uint32_t>(1, std::min<uint32_t>(ceil_div(L->ns, want), 2));
-            if (const char* e = std::getenv("DSQ_K8_SPANS")) L->batch_spans = std::max(1, atoi(e));
-            L->batch_kslices = ceil_div(L->ns, L->batch_spans);
-            // + the transposed x [ns * 256 cols][16] halves for the CSR gathers
-            CUDA_TRY(cudaMalloc(&L->batch_part,
-                                size_t(L->batch_kslices) * tiles16 * 16 * 16 * sizeof(float) +
-                                    size_t(L->ns) * kSpanCols * 16 * sizeof(uint16_t)));
-        }
+        const int rc = ensure_bstream(L, nb);
+        if (rc) return rc;
     }
-    CUDA_TRY(launch_batch(L->bits, L->rec, L->tlut, L->P.row_ptr, L->P.csr, L->rows, L->cols,
-                          L->ns, L->tiles, static_cast<const uint16_t*>(x), x_stride, batch, y,
-                          y_stride, y_dtype == DSQ_F16, L->batch_part, L->batch_kslices,
-                          L->batch_spans, mode, st));
+    CUDA_TRY(launch_bstream(L->bits, nb, L->bs[nb - 1], L->rec, L->tlut, L->P.row_ptr, L->P.csr,
+                            L->rows, L->cols, L->ns, L->tiles, static_cast<const uint16_t*>(x),
+                            x_stride, batch, y, y_stride, y_dtype == DSQ_F16, mode, st));
     return DSQ_OK;
 }
 
@@ -1114,9 +1069,9 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
                 StackPlanLayer pl{L->rows, L->cols, L->tiles, L->ns,
                                   max_nnz_per_cta(L->row_ptr_host, L->rows, L->num_sms)};
                 int prc = plan_stack(&pl, 1, L->num_sms, L->bits, spb, gcap, nb);
-                if (prc == DSQ_E_UNSUPPORTED) {  // the x vectors do not fit: the K8 path
+                if (prc == DSQ_E_UNSUPPORTED) {  // the x vectors do not fit: the K11 path
                     (nb == 2 ? L->sp2_failed : nb == 4 ? L->sp4_failed : L->sp8_failed) = true;
-                    goto batched_k8;
+                    goto batched_k11;
                 }
                 if (prc) return prc;
                 if (gcap)
@@ -1155,7 +1110,7 @@ static int gemv_impl(const dsq_cuda_layer* Lc, int kernel, const void* x, int x_
         CUDA_TRY(launch_stack(sp, st, pdl));
         return DSQ_OK;
     }
-batched_k8:
+batched_k11:
     if (batch > 1)
         return gemv_batch(L, kernel, x, x_dtype, y, y_dtype, batch, st, x_stride, y_stride);
     if (kernel < DSQ_KERNEL_LUT || kernel > DSQ_KERNEL_REFERENCE)

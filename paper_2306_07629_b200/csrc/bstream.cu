@@ -2,11 +2,18 @@
 // B = 5..16 activation vectors (BASELINE configs[4]) on per-warp TMA rings.
 //
 // Same HBM layout as the batch-1 kernel (stack.hpp: 4-row tiles, 256-column
-// spans) read with the DENSE fragment map of K8 (batch.cu): a warp decodes a
-// 16-row tile (4 consecutive 4-row tiles) and every mma.sync.m16n8k16 uses all
-// 16 A rows and all 8 B columns = 8 batch vectors, so one decoded weight feeds
-// up to 16 products for the tensor cost of batch 1 (B <= 8: 4 HMMA per 1024
-// weights, as the batch-1 block-diagonal map; B <= 16: 8).
+// spans) read with a DENSE fragment map: a warp decodes a 16-row tile (4
+// consecutive 4-row tiles) and every mma.sync.m16n8k16 uses all 16 A rows and
+// all 8 B columns = 8 batch vectors, so one decoded weight feeds up to 16
+// products for the tensor cost of batch 1 (B <= 8: 4 HMMA per 1024 weights,
+// as the batch-1 block-diagonal map; B <= 16: 8).
+//
+//   thread (g, t): A rows g and g+8 = tile rows 16q + g and 16q + g + 8, i.e.
+//   4-row tiles j0 = g / 4 and j0 + 2, tile row g % 4; it reads the two lanes
+//   (h = 0/1, i = g % 4, t) of each of those tiles' units, 64 indices per row
+//   per span = 16 quads; HMMA m takes quad m of both rows as its k-slots (2t,
+//   2t+1, 2t+8, 2t+9) and x[vector g] at the quad's 4 columns as its B
+//   fragment.  D[g][n] / D[g+8][n] are rows x vector n.
 //
 // Work split (host plan, bstream_plan below).  The columns are cut in PHASES
 // of at most 8 (B > 8) or 16 spans, so one phase's x for all 8*NB vectors is
@@ -72,7 +79,8 @@ SQZ_HD inline uint32_t bs_pack_w(uint32_t phase, uint32_t a, uint32_t gp) {
     return phase | (a << 8) | (gp << 20);
 }
 
-// lane_quads / quad_col: batch.cu
+// one lane's 32 indices of a unit -> 8 quads (selector words in the low 16
+// bits; 4-bit: the pick words for the upper half table)
 template <int BITS>
 __device__ __forceinline__ void bs_quads(const uint32_t* w, uint32_t (&q)[8], uint32_t (&pk)[8]) {
     if constexpr (BITS == 3) {
@@ -323,8 +331,7 @@ __global__ void __launch_bounds__(W * 32, 1) bstream_gemv(const __grid_constant_
 // then added in a fixed shuffle order (deterministic).  All loads that do not
 // depend on each other are issued together: the row pointers and the
 // phases' segment bounds in one round trip, then the segments and the CSR
-// entries, then the transposed x (as batch_finish in batch.cu, but ~3 dependent
-// round trips per row instead of ~5).
+// entries, then the transposed x.
 template <int XB>
 __global__ void __launch_bounds__(256) bstream_finish(const float* __restrict__ part, const uint32_t* __restrict__ seg_base,
                                uint32_t phases, uint32_t tiles16, uint32_t rows, uint32_t B,

@@ -15,9 +15,9 @@
 
 namespace sqz {
 
-// phases carried in the launch parameters (wider layers: more than 24 * 8
-// spans at B > 8 -- use the K8 path)
-constexpr uint32_t kBsMaxPhases = 24;
+// phases carried in the launch parameters: 32 covers every layer the tile
+// layout holds (cols < 65536 = 256 spans, 8 spans per phase at B > 8)
+constexpr uint32_t kBsMaxPhases = 32;
 
 // the cell range [*wb, *we) of warp w of CTA `cta` (phase tables as in
 // BStreamPlanHost): the kernel derives its range from the launch parameters
