@@ -255,20 +255,22 @@ int dsq_cuda_stack_run(dsq_cuda_stack* stack, void* stream);
  * completion ends step k (values 1, 2, .. K in layer order, 0 elsewhere).
  *   dsq_cuda_serve_begin: launch (the kernel streams the weights and waits at
  *     the first gate); x_bytes (multiple of 16) per step go to x_dev, and the
- *     first y_bytes of each notify layer's output (device buffer, 16-byte
- *     aligned) are copied by CTA 0 into y_host (pinned) before the step is
- *     announced -- read them after dsq_cuda_serve_step returns;
+ *     first y_bytes of each notify layer's output (16-byte aligned) reach
+ *     y_host (any host memory) -- read them after dsq_cuda_serve_step returns;
  *   dsq_cuda_serve_step: copy x_host into a pinned staging buffer and ring
  *     step k's doorbell (host memory); CTA 0 of the kernel copies the bytes
- *     over PCIe into x_dev and releases the grid; returns once the kernel's
- *     completion word for step k has arrived in host memory;
+ *     over PCIe into x_dev and releases the grid; the notify layer's
+ *     finishing warps write their rows straight into pinned host memory as
+ *     64-bit {4 payload bytes, tag k} words (no fence, no gather); returns
+ *     once every word of step k carries its tag, the payloads copied into
+ *     y_host (with y_bytes = 0: once the kernel's completion word arrives);
  *   dsq_cuda_serve_end: release any steps not fed, wait for the launch.
  * Gated layers of step k must sit after notify k-1 and before notify k
  * (gate[i] == 1 + the notify layers before i) and share one x buffer of
  * their common cols; x_bytes must be cols*2 rounded up to at most 16.  The
  * kernel waits for a step's doorbell without a timeout (an idle server may
  * wait any time; it never computes on a stale x); dsq_cuda_serve_step gives
- * up with DSQ_E_INTERNAL after 10 s without the step's completion word, and
+ * up with DSQ_E_INTERNAL after 10 s without the step's outputs, and
  * dsq_cuda_serve_end releases the steps not fed.  Single GPU, batch 1;
  * dsq_cuda_stack_run is refused on a served stack. */
 int dsq_cuda_stack_create_served(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,

@@ -1487,6 +1487,9 @@ struct dsq_cuda_stack {
     uint32_t* serve_dev = nullptr;
     uint32_t* serve_pin = nullptr;
     void* serve_x_pin = nullptr;  // pinned, device-mapped x staging
+    void* serve_ll_pin = nullptr;  // pinned, device-mapped tagged output words
+    size_t serve_ll_cap = 0;
+    uint32_t* serve_y_host = nullptr;  // the caller's output buffer (serve_begin)
     size_t serve_x_cap = 0, serve_x_bytes = 0;
     size_t serve_y_cap = 0;  // bytes of the smallest notify layer's y (0: unaligned)
     const void* serve_x_ptr = nullptr;  // the gated layers' (common) x buffer
@@ -1980,19 +1983,33 @@ int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* y
     if (y_bytes % 16 || (y_bytes && (!y_host || (reinterpret_cast<uintptr_t>(y_host) & 15u))))
         return fail(DSQ_E_INVALID_ARGUMENT, "serve: y_host / y_bytes must be 16-byte aligned");
     cudaSetDevice(S->device);
-    S->sp.serve_y_dst = nullptr;
-    S->sp.serve_y_bytes = 0;
+    S->sp.serve_y_ll = nullptr;
+    S->sp.serve_y_words = 0;
+    S->serve_y_host = nullptr;
     if (y_bytes) {
         if (y_bytes > S->serve_y_cap)
             return fail(DSQ_E_INVALID_ARGUMENT,
                         "serve: y_bytes > a notify layer's output (or its y is not 16-byte aligned)");
-        void* y_map = nullptr;
-        CUDA_TRY(cudaHostGetDevicePointer(&y_map, y_host, 0));
-        S->sp.serve_y_dst = static_cast<uint4*>(y_map);
-        S->sp.serve_y_bytes = uint32_t(y_bytes);
+        // the kernel's tagged output words (4 payload bytes each), cleared so
+        // no tag of an earlier session matches
+        const size_t ll_bytes = y_bytes * 2;
+        if (S->serve_ll_cap < ll_bytes) {
+            if (S->serve_ll_pin) cudaFreeHost(S->serve_ll_pin);
+            S->serve_ll_pin = nullptr;
+            S->serve_ll_cap = 0;
+            CUDA_TRY(cudaHostAlloc(&S->serve_ll_pin, ll_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+            S->serve_ll_cap = ll_bytes;
+        }
+        std::memset(S->serve_ll_pin, 0, ll_bytes);
+        void* ll_map = nullptr;
+        CUDA_TRY(cudaHostGetDevicePointer(&ll_map, S->serve_ll_pin, 0));
+        S->sp.serve_y_ll = static_cast<unsigned long long*>(ll_map);
+        S->sp.serve_y_words = uint32_t(y_bytes / 4);
+        S->serve_y_host = static_cast<uint32_t*>(y_host);
     }
     if (S->serve_x_cap < x_bytes) {
         if (S->serve_x_pin) cudaFreeHost(S->serve_x_pin);
+    if (S->serve_ll_pin) cudaFreeHost(S->serve_ll_pin);
         S->serve_x_pin = nullptr;
         S->serve_x_cap = 0;
         CUDA_TRY(cudaHostAlloc(&S->serve_x_pin, x_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -2025,14 +2042,29 @@ int dsq_cuda_serve_step(dsq_cuda_stack* S, const void* x_host) {
     std::memcpy(S->serve_x_pin, x_host, S->serve_x_bytes);
     std::atomic_thread_fence(std::memory_order_seq_cst);
     reinterpret_cast<volatile uint32_t*>(S->serve_pin)[1] = k;
-    const volatile uint32_t* done = S->serve_pin;
     const auto t0 = std::chrono::steady_clock::now();
     uint32_t spins = 0;
-    while (*done < k) {
-        if ((++spins & 1023u) == 0 &&
-            std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
-            return fail(DSQ_E_INTERNAL, "serve: step %u did not complete in 10 s", k);
+    auto late = [&]() {
+        return (++spins & 1023u) == 0 &&
+               std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10);
+    };
+    if (S->serve_y_host) {
+        // the step's output words, tag k each (written by the finishing warps
+        // of the notify layer, no fence): spin per word, keep the payload
+        const volatile unsigned long long* ll =
+            static_cast<const volatile unsigned long long*>(S->serve_ll_pin);
+        const uint32_t nw = S->sp.serve_y_words;
+        for (uint32_t w = 0; w < nw; ++w) {
+            unsigned long long v;
+            while (uint32_t((v = ll[w]) >> 32) != k)
+                if (late()) return fail(DSQ_E_INTERNAL, "serve: step %u did not complete in 10 s", k);
+            S->serve_y_host[w] = uint32_t(v);
+        }
+        return DSQ_OK;
     }
+    const volatile uint32_t* done = S->serve_pin;
+    while (*done < k)
+        if (late()) return fail(DSQ_E_INTERNAL, "serve: step %u did not complete in 10 s", k);
     std::atomic_thread_fence(std::memory_order_acquire);
     return DSQ_OK;
 }
@@ -2056,6 +2088,7 @@ int dsq_cuda_stack_destroy(dsq_cuda_stack* S) {
         dsq_cuda_serve_end(S);
     }
     if (S->serve_x_pin) cudaFreeHost(S->serve_x_pin);
+    if (S->serve_ll_pin) cudaFreeHost(S->serve_ll_pin);
     if (S->serve_pin) cudaFreeHost(S->serve_pin);
     if (S->serve_dev) cudaFree(S->serve_dev);
     if (S->arena) cudaFree(S->arena);

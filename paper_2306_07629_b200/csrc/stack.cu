@@ -503,14 +503,30 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                 }
                 sv[v - 1] = t;
             }
-            if (i >= nrows) continue;  // padding rows of the last tile
-            const uint32_t a = rp[i] - ea, e = rp[i + 1] - ea;
+            const bool valid = i < nrows;  // else a padding row of the last tile
+            const uint32_t a = valid ? rp[i] - ea : 0u, e = valid ? rp[i + 1] - ea : 0u;
             for (uint32_t j = a / 128; e > a && j <= (e - 1) / 128; ++j) {
                 const uint32_t q = j * 128 + min(e - 1 - j * 128, 127u);
                 s += S[q];
 #pragma unroll
                 for (int v = 1; v < NB; ++v) sv[v - 1] += S[v * s_vec + q];
             }
+            if (SERVE && p.serve_y_words && p.serve_notify[l]) {
+                // served output: rows 2j / 2j+1 sit in lanes 2m / 2m+1 (r0 is a
+                // multiple of 4, the row stride 32 * kFin even), both live or
+                // both past the loop end
+                const unsigned long long tag = static_cast<unsigned long long>(p.serve_notify[l]) << 32;
+                if (d.y_f16) {
+                    const uint32_t h = valid ? uint32_t(__half_as_ushort(__float2half_rn(s))) : 0u;
+                    const uint32_t h1 = __shfl_down_sync(__activemask(), h, 1);
+                    const uint32_t w = (r0 + i) >> 1;
+                    if (valid && !(lane & 1u) && w < p.serve_y_words)
+                        st_volatile_u64(p.serve_y_ll + w, tag | (h1 << 16) | h);
+                } else if (valid && r0 + i < p.serve_y_words) {  // fp32: one row per word
+                    st_volatile_u64(p.serve_y_ll + r0 + i, tag | __float_as_uint(s));
+                }
+            }
+            if (!valid) continue;
 #pragma unroll
             for (int v = 1; v < NB; ++v) {
                 if (uint32_t(v) >= p.nvec) continue;
@@ -584,29 +600,11 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             if (f == 0 && lane == 0) red_release_gpu_add(p.counters + l, 1u);
         }
         if (f == 0 && lane == 0) DSQ_TRACE(l, kTrSignaled);
-        if (notify && f == 0 && cta == 0) {
-            // every finishing warp of every CTA is done: copy step `notify`'s
-            // output to the host (one burst of PCIe writes), then announce it
-            if (lane == 0)
-                while (ld_acquire_gpu(p.counters + l) < G * sig_per_cta) __nanosleep(32);
-            __syncwarp();
-            const uint32_t n16 = p.serve_y_bytes / 16;
-            const uint4* ysrc = static_cast<const uint4*>(d.y);
-            for (uint32_t i0 = 0; i0 < n16; i0 += 32 * 16) {
-                uint4 v[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const uint32_t i = i0 + 32 * u + lane;
-                    if (i < n16) v[u] = ld_cg_v4(ysrc + i);
-                }
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const uint32_t i = i0 + 32 * u + lane;
-                    if (i < n16) p.serve_y_dst[i] = v[u];
-                }
-            }
-            __syncwarp();
+        if (notify && f == 0 && cta == 0 && !p.serve_y_words) {
+            // no output buffer: announce the step once every finishing warp
+            // of every CTA is done
             if (lane == 0) {
+                while (ld_acquire_gpu(p.counters + l) < G * sig_per_cta) __nanosleep(32);
                 __threadfence_system();
                 st_release_sys(p.host_done, notify);
             }

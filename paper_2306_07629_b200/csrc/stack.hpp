@@ -134,10 +134,12 @@ struct StackParams {
     // doorbell (*doorbell >= k, pinned host memory), copies the step's x from
     // the pinned staging buffer into serve_x_dst (the layer's x) over PCIe and
     // publishes *serve_flag = k; the other CTAs wait for the flag.  For a
-    // layer with serve_notify[l] = k > 0 every finishing warp fences its rows
-    // of y system-wide before its completion release, and CTA 0 waits for the
-    // layer's count, copies the layer's y (device memory) into serve_y_dst
-    // over PCIe and stores k into *host_done (pinned host memory).  No CUDA
+    // layer with serve_notify[l] = k > 0 (fp16 y) every finishing warp
+    // writes its rows straight into host memory as 64-bit words {two fp16
+    // rows, tag k} (serve_y_ll, single-copy atomic: no fence, no gather --
+    // the host polls the tags, NCCL's LL protocol idea); without an output
+    // buffer CTA 0 waits for the layer's count, fences and stores k into
+    // *host_done (pinned host memory).  No CUDA
     // call per step on the host.  The gate waits have no timeout (an idle
     // server may wait any time; a stale x is never computed on): only the
     // host's doorbell or serve_end's release (0xffffffff) ends them.
@@ -148,8 +150,8 @@ struct StackParams {
     uint4* serve_x_dst;
     uint32_t serve_x_bytes;       // multiple of 16
     uint32_t* serve_flag;         // device word: the step whose x is in serve_x_dst
-    uint4* serve_y_dst;           // device-mapped pinned host: a notify layer's y copy
-    uint32_t serve_y_bytes;       // (0: none; multiple of 16)
+    unsigned long long* serve_y_ll;  // device-mapped pinned host: {rows 2j, 2j+1, tag} words
+    uint32_t serve_y_words;       // rows / 2 of the notify layer's y sent (0: none)
     uint32_t* host_done;          // device-mapped pinned host word
     uint32_t* serve_err;
 };
