@@ -126,6 +126,10 @@ typedef struct dsq_layer_info {
 int dsq_cuda_abi_version(void);
 /* thread-local message for the last non-OK status (never NULL) */
 const char* dsq_cuda_last_error(void);
+/* The CUDA runtime's pending (non-sticky) error of the calling thread, cleared
+ * by the call: 0 when none.  Diagnostics -- every entry point above checks and
+ * reports its own CUDA calls. */
+int dsq_cuda_pending_error(void);
 
 /* ---- layer lifetime ----------------------------------------------------- */
 /* Validates the view exactly like QuantizedLayer::validate()

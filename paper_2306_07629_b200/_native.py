@@ -115,6 +115,7 @@ class QuantConfig(C.Structure):
 PROTOTYPES = {
     "dsq_cuda_abi_version": (C.c_int, []),
     "dsq_cuda_last_error": (C.c_char_p, []),
+    "dsq_cuda_pending_error": (C.c_int, []),
     "dsq_cuda_layer_create": (C.c_int, [C.POINTER(LayerView), C.c_int, C.POINTER(C.c_void_p)]),
     "dsq_cuda_layer_destroy": (C.c_int, [C.c_void_p]),
     "dsq_cuda_layer_get_info": (C.c_int, [C.c_void_p, C.POINTER(LayerInfo)]),

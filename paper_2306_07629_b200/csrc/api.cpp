@@ -425,6 +425,7 @@ extern "C" {
 int dsq_cuda_abi_version(void) { return DSQ_CUDA_ABI_VERSION; }
 
 const char* dsq_cuda_last_error(void) { return g_err.c_str(); }
+int dsq_cuda_pending_error(void) { return int(cudaGetLastError()); }
 
 uint64_t dsq_bytes_touched_estimate(uint32_t rows, uint32_t cols, uint32_t bits,
                                     uint32_t group_size, uint64_t nnz) {
@@ -2009,7 +2010,6 @@ int dsq_cuda_serve_begin(dsq_cuda_stack* S, void* x_dev, size_t x_bytes, void* y
     }
     if (S->serve_x_cap < x_bytes) {
         if (S->serve_x_pin) cudaFreeHost(S->serve_x_pin);
-    if (S->serve_ll_pin) cudaFreeHost(S->serve_ll_pin);
         S->serve_x_pin = nullptr;
         S->serve_x_cap = 0;
         CUDA_TRY(cudaHostAlloc(&S->serve_x_pin, x_bytes, cudaHostAllocMapped | cudaHostAllocPortable));

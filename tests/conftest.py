@@ -40,3 +40,16 @@ def torch():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch
+
+
+@pytest.fixture(autouse=True)
+def _no_pending_cuda_error(request):
+    """Every GPU test must leave the library's CUDA runtime without a pending
+    error (an unchecked failing call would otherwise surface in a later,
+    unrelated launch)."""
+    yield
+    if request.node.get_closest_marker("gpu") is None or not has_gpu():
+        return
+    import paper_2306_07629_b200._native as N
+    code = N.lib.dsq_cuda_pending_error()
+    assert code == 0, f"pending CUDA error {code} after {request.node.name}"
