@@ -327,8 +327,9 @@ __global__ void __launch_bounds__(W * 32, 1) bstream_gemv(const __grid_constant_
 
 // y[b][r] = the row's segments + its CSR deltas.  One warp per row: lane =
 // part * XB + b (XB = 8 * NB, P = 32 / XB parts).  Part k sums every P-th
-// segment of each phase and every P-th group of 8 CSR entries; the parts are
-// then added in a fixed shuffle order (deterministic).  All loads that do not
+// segment of each phase and every P-th CSR entry (entries in rounds of 32,
+// one coalesced load per round); the parts are then added in a fixed shuffle
+// order (deterministic).  All loads that do not
 // depend on each other are issued together: the row pointers and the
 // phases' segment bounds in one round trip, then the segments and the CSR
 // entries, then the transposed x.
@@ -366,24 +367,29 @@ __global__ void __launch_bounds__(256) bstream_finish(const float* __restrict__ 
     }
     if (with_csr) {
         const uint32_t q0 = __shfl_sync(0xffffffffu, rp, 30), q1 = __shfl_sync(0xffffffffu, rp, 31);
-        if (b < B) {
-            const uint16_t* xb = xT ? xT + b : x + size_t(b) * x_stride;
-            const uint32_t xs = xT ? uint32_t(XB) : 1u;
-            float c = 0.f;
-            for (uint32_t q = q0 + 8 * k; q < q1; q += 8 * P) {
-                uint32_t e[8];
+        const bool live = b < B;
+        const uint16_t* xb = xT ? xT + (live ? b : 0u) : x + size_t(live ? b : 0u) * x_stride;
+        const uint32_t xs = xT ? uint32_t(XB) : 1u;
+        constexpr uint32_t U = 32 / P;  // entries per lane per round of 32
+        float c = 0.f;
+        // rounds of 32 entries: one coalesced load (an entry per lane), then
+        // part k gathers x for entries k, k + P, .. -- all in flight together
+        for (uint32_t base = q0; base < q1; base += 32) {
+            const uint32_t n = min(32u, q1 - base);
+            const uint32_t ent = lane < n ? __ldg(csr + base + lane) : 0u;
+            uint32_t ev[U];
+            uint16_t xv[U];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) e[u] = q + u < q1 ? __ldg(csr + q + u) : 0u;
-                uint16_t xv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    xv[u] = q + u < q1 ? ld_cg_u16(xb + size_t(e[u] & 0xffffu) * xs) : uint16_t(0);
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (q + u < q1) c = fma_h(uint16_t(e[u] >> 16), xv[u], c);
+            for (uint32_t u = 0; u < U; ++u) {
+                const uint32_t j = u * P + k;
+                ev[u] = __shfl_sync(0xffffffffu, ent, j);
+                xv[u] = live && j < n ? ld_cg_u16(xb + size_t(ev[u] & 0xffffu) * xs) : uint16_t(0);
             }
-            s += c;
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u)
+                if (live && u * P + k < n) c = fma_h(uint16_t(ev[u] >> 16), xv[u], c);
         }
+        s += c;
     }
 #pragma unroll
     for (uint32_t o = XB; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
