@@ -955,6 +955,19 @@ def run_ours_tp(args, rank: int, world: int, local_rank: int):
         "e2e": e2e, "clocks": clocks, "gpu_launches": 1, "gemvs_timed": args.steps * 7,
         "mode": "stack-tp", "setup_s": round(setup_s, 1),
     }
+    if world > 1 and model == "65b":
+        # `bench.py --gpus 1` measures BASELINE configs[1] (the 7B chain); the
+        # same 65B chain on one GPU (`--workload 65b`), for a same-workload
+        # scaling read, is the builder's committed measurement
+        ref1 = ROOT / "profiles" / "r02_bench_65b_tp1.json"
+        if ref1.exists():
+            try:
+                v1 = json.loads(ref1.read_text())["value"]
+                line["same_workload_1gpu"] = {
+                    "value": v1, "unit": "GB/s", "source": str(ref1.relative_to(ROOT)),
+                    "note": "python bench.py --workload 65b at N = 1 (not this run)"}
+            except Exception:
+                pass
     print(json.dumps(line), flush=True)
 
 
