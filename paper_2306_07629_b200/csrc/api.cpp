@@ -246,6 +246,8 @@ void fill_desc(StackLayerDesc& d, const StackPlanLayer& l, uint32_t slot_bytes, 
     }
 }
 
+constexpr uint64_t kRingGrowUnits = 250;  // see plan_stack (ring chunk size)
+
 int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, StackParams& sp,
                uint32_t& gseg_cap, uint32_t nbatch = 1, bool x_shared = false) {
     int dev = 0, smax = 0;
@@ -298,11 +300,18 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
     sp.off_x = uint32_t(off);
     sp.nbatch = nbatch;
     sp.nvec = nbatch;
-    sp.xvec = uint32_t(al(size_t(max_ns) * kSpanCols * 2, 128) / 2);  // halves per vector
+    sp.xvec = uint32_t(size_t(max_ns) * kSpanCols);  // halves per vector, largest layer
     sp.x_bytes = uint32_t(size_t(sp.xvec) * 2 * nbatch);
-    const size_t nbuf_x = x_shared ? 1 : nbuf;
-    sp.x_step = nbuf_x == 2 ? sp.x_bytes : 0u;
-    off += nbuf_x * size_t(sp.x_bytes);
+    // x: layer l takes ns_l * 256 halves per vector; two consecutive layers
+    // must coexist (layer l+1's x is staged while layer l decodes): a region
+    // of the largest consecutive pair, even layers at its bottom, odd at its
+    // top (stack.cu x_region) -- not two buffers of the largest layer
+    size_t x_pair = 0;
+    for (uint32_t i = 1; i < n; ++i)
+        x_pair = std::max(x_pair, (size_t(Ls[i - 1].ns) + Ls[i].ns) * kSpanCols * 2 * nbatch);
+    const bool two = nbuf == 2 && !x_shared;
+    sp.x_step = two ? uint32_t(x_pair) : 0u;
+    off += two ? x_pair : size_t(sp.x_bytes);
     sp.off_lut = uint32_t(off);
     sp.lut_bytes = uint32_t(al(size_t(max_rows) * tile_lut_words(bits) * 4, 128));
     off += nbuf * size_t(sp.lut_bytes);
@@ -332,6 +341,19 @@ int plan_stack(const StackPlanLayer* Ls, uint32_t n, int G, uint32_t bits, Stack
         ws = std::max<uint32_t>(2, std::min<uint32_t>(kMaxWarpSlots, uint32_t(atoi(e))));
     sp.n_slots = sp.consumers * ws;
     sp.slot_bytes = uint32_t(ring / sp.n_slots / ub * ub);
+    if (two) {
+        // small layers (mean units per CTA < kRingGrowUnits, the LLaMA-7B
+        // chain) keep the chunk size of two full-size x buffers: measured
+        // -1% on the 7B chain with the larger chunks the pair-sized region
+        // frees, +4% on the 13B / 65B stacks (larger layers)
+        uint64_t units = 0;
+        for (uint32_t i = 0; i < n; ++i) units += uint64_t(ceil_div(Ls[i].tiles, G)) * Ls[i].ns;
+        const size_t freed = 2 * size_t(sp.x_bytes) - x_pair;
+        if (units < kRingGrowUnits * n && ring > freed) {
+            const uint32_t old_slot = uint32_t((ring - freed) / sp.n_slots / ub * ub);
+            if (old_slot >= 2 * ub) sp.slot_bytes = old_slot;
+        }
+    }
     if (sp.slot_bytes < 2 * ub) {
         // large batched x: retry with one shared x buffer before giving up
         if (nbatch > 1 && nbuf == 2 && !x_shared)

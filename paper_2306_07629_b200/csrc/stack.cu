@@ -67,6 +67,16 @@ __device__ __forceinline__ const StackLayerDesc& layer_desc(const StackParams& p
     return l < kInlineLayers && p.n_layers <= kInlineLayers ? p.inl[l] : p.layers[l];
 }
 
+// layer l's x in shared memory: p.x_step != 0 -> a region of x_step bytes
+// with even layers at its bottom and odd layers at its top (the host sizes it
+// for the largest pair of consecutive layers, so layer l's x never overlaps
+// layer l-1's; it may overlap l-2's, whose readers the loader waits for
+// through bempty, as with two fixed buffers); 0 -> one shared buffer.  Each
+// of the NB vectors takes ns * 256 halves.
+__device__ __forceinline__ uint32_t x_region(const StackParams& p, uint32_t l, uint32_t ns) {
+    return (p.x_step && (l & 1u)) ? p.x_step - ns * kSpanCols * 2u * p.nbatch : 0u;
+}
+
 // CTA tile share from the host-precomputed quotient/remainder (no division)
 struct Share {
     uint32_t t0, nt;       // first tile, tiles
@@ -330,7 +340,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             const StackLayerDesc& d = sd.d;
             const Share sh = cta_share(d, cta);
             const uint32_t r0 = sh.r0, r1 = sh.r0 + sh.nrows;
-            uint8_t* xb = sm + p.off_x + b * p.x_step;
+            uint8_t* xb = sm + p.off_x + x_region(p, l, d.ns);
+            const uint32_t xvl = d.ns * kSpanCols;  // halves per vector
             if (lane == 0) {
                 DSQ_TRACE(l, kTrLoaderStart);
                 // the CTA's LUT planes ride on the x barrier (expected first,
@@ -355,7 +366,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
 #pragma unroll
                 for (int v = 0; v < NB; ++v) {  // batch vector v at xb + v * xvec halves
                     if (uint32_t(v) >= nv) continue;
-                    uint16_t* xv = reinterpret_cast<uint16_t*>(xb) + v * p.xvec;
+                    uint16_t* xv = reinterpret_cast<uint16_t*>(xb) + v * xvl;
                     const uint16_t* gx = d.x + size_t(v) * xstride;
                     for (uint32_t i = body / 2 + lane; i < d.ns * kSpanCols; i += 32)
                         xv[i] = i < d.cols ? ld_cg_u16(gx + i) : uint16_t(0);
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
 #pragma unroll
                         for (int v = 0; v < NB; ++v)
                             if (uint32_t(v) < nv)
-                                bulk_g2s_plain(reinterpret_cast<uint16_t*>(xb) + v * p.xvec,
+                                bulk_g2s_plain(reinterpret_cast<uint16_t*>(xb) + v * xvl,
                                                d.x + size_t(v) * xstride, body, &xfull[b]);
                 }
             };
@@ -651,7 +662,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
             mbar_wait_fin(&cfull[b], ph);
             if (l >= 2) mbar_wait_fin(&pempty[b], ((l >> 1) - 1) & 1u);  // segs consumed
             if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrCsrStaged);
-            const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);
+            const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + x_region(p, l, sd.d.ns));
+            const uint32_t xvl = sd.d.ns * kSpanCols;
             const uint32_t* rp = reinterpret_cast<const uint32_t*>(sm + p.off_rp) + b * p.rp_words;
             (void)rp;
             const uint32_t e0 = sd.e0, e1 = sd.e1, ea = e0 & ~3u;
@@ -668,7 +680,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
 #pragma unroll
                 for (int v = 0; v < NB; ++v)
                     if (v == 0 || uint32_t(v) < p.nvec)
-                        csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh + v * p.xvec,
+                        csr_stream(ea, e0, e1, ent, hb, hbase, hlast, xh + v * xvl,
                                    S + v * (staged ? p.seg_cap : p.gseg_cap), cw, p.csr_warps, lane);
             }
             __syncwarp();
@@ -688,7 +700,7 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
     const uint32_t cw = warp;
     // this lane's B-column x halves (NB == 2: B columns 4..7, lanes 16..31,
     // read batch vector 1)
-    const uint32_t xoff = tile_x_offset(lane) + (NB >= 2 ? (lane >> 4) * p.xvec : 0u);
+    const uint32_t xoff0 = tile_x_offset(lane);  // + the lane's vector (per layer)
     const uint32_t trow = (lane >> 2) & 3u;         // tile row of this lane
     const ShiftK K{p.k29, p.k30, p.k31, p.kneg};
     const uint64_t policy = policy_evict_first();
@@ -768,7 +780,9 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
         if (l >= 2) mbar_wait_edge(&pempty[b], ((l >> 1) - 1) & 1u);
         DSQ_LAP(c_xw);
         if (cw == 0 && lane == 0) DSQ_TRACE(l, kTrXReady);
-        const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + b * p.x_step);
+        const uint16_t* xh = reinterpret_cast<const uint16_t*>(sm + p.off_x + x_region(p, l, d.ns));
+        const uint32_t xvl = d.ns * kSpanCols;  // halves per vector in this layer's x
+        const uint32_t xoff = xoff0 + (NB >= 2 ? (lane >> 4) * xvl : 0u);
         const uint32_t* luts = reinterpret_cast<const uint32_t*>(sm + p.off_lut + b * p.lut_bytes);
         float* part = reinterpret_cast<float*>(sm + p.off_part) + size_t(b) * NB * p.part_rows * NC;
 
@@ -876,8 +890,8 @@ __global__ void __launch_bounds__((NC + 3 + kCsrWarps) * 32, 1)
                             uint4 ya[NX], yb[NX];
 #pragma unroll
                             for (int q = 0; q < NX; ++q) {
-                                ya[q] = *reinterpret_cast<const uint4*>(xs + 2 * (q + 1) * p.xvec);
-                                yb[q] = *reinterpret_cast<const uint4*>(xs + 2 * (q + 1) * p.xvec + 128);
+                                ya[q] = *reinterpret_cast<const uint4*>(xs + 2 * (q + 1) * xvl);
+                                yb[q] = *reinterpret_cast<const uint4*>(xs + 2 * (q + 1) * xvl + 128);
                             }
                             if constexpr (BITS == 3) {
                                 span3_mma_xn<NX>(sp[lane], sp[32 + lane], sp[64 + lane], P.a, xa0,
