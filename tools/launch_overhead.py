@@ -1,5 +1,17 @@
-import sys, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+"""Fixed cost of an isolated persistent-kernel launch (dev tool): 200
+single-layer fused products (K7, one launch each) of a small, a medium and a
+4096^2 3-bit layer, back to back in one captured CUDA graph, rotating over 8
+device copies; prints microseconds per launch (3.46 us
+for 128x256).
+
+usage: python tools/launch_overhead.py"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2306_07629_b200._native as N
 from paper_2306_07629_b200 import DeviceLayer
 from oracle.oracle import make_layer, make_x, to_quantized_layer
