@@ -143,7 +143,12 @@ int dsq_cuda_layer_get_info(const dsq_cuda_layer* layer, dsq_layer_info* info);
 
 /* ---- products (device buffers, stream-ordered) -------------------------- */
 /* y[r] (rows) = product of row r with x (cols).  x_dtype F32/F16 (F32 is
- * rounded to fp16 on device), y_dtype F32/F16.  batch must be 1 in ABI v1.
+ * rounded to fp16 on device), y_dtype F32/F16.  batch 1..16 (bits 3/4): x
+ * [batch][cols] F16 with 16-byte aligned rows, y [batch][rows]; batch 2..4
+ * run on the persistent kernel with every decoded weight shared by all
+ * vectors, 5..16 on the batched LUT-GEMM K11 plus its finish kernel (two
+ * launches; a layer's batched scratch is reused, so one batched product per
+ * layer at a time, in stream order).
  * Replaces:
  *   DSQ_KERNEL_LUT   -> dsq::lut_matvec        kernels.hpp:20 / kernels.cpp:51-67
  *   DSQ_KERNEL_CSR   -> dsq::csr_matvec        kernels.hpp:24 / kernels.cpp:69-85
@@ -244,8 +249,10 @@ int dsq_cuda_stack_create(dsq_cuda_layer* const* layers, uint32_t n, const int32
  * cols / rows).  Every decoded weight is shared by all vectors (batch 2: the
  * spare HMMA B columns; 3..4: a second HMMA per fragment).  Batches of 5..16,
  * or of 2..4 whose x vectors do not fit next to the persistent kernel's ring,
- * run in the sequential form: one batched product launch per layer, back to
- * back under programmatic dependent launch (dsq_cuda_stack_info).  Single GPU. */
+ * run in the sequential form: one batched product per layer, back to back
+ * under programmatic dependent launch, captured into a CUDA graph during the
+ * first run and replayed as one graph launch afterwards (dsq_cuda_stack_info).
+ * Single GPU. */
 int dsq_cuda_stack_create_batch(dsq_cuda_layer* const* layers, uint32_t n, const int32_t* deps,
                                 const void* const* xs, void* const* ys, int y_dtype,
                                 uint32_t batch, uint32_t x_bstride, uint32_t y_bstride,
