@@ -44,6 +44,9 @@ def shapes(h, f):
             ("down", h, f)]
 
 
+SPARSITY_ARG = 0.0045  # --sparsity
+
+
 def fast_layer(rows, cols, bits=3, sparsity=0.0045, seed=0):
     from paper_2306_07629_b200 import CsrMatrix, PackedDense, QuantizedLayer
     from oracle.oracle import nnz_for
@@ -81,7 +84,7 @@ def run(model, tokens, rotation, peak, rank=0, world=1, batch=1):
     cache, qls, nnzs = {}, [], []
     for name, r, c in shp:
         if (r, c) not in cache:
-            cache[(r, c)] = fast_layer(r, c, seed=r * 7 + c)
+            cache[(r, c)] = fast_layer(r, c, sparsity=SPARSITY_ARG, seed=r * 7 + c)
         q, nz = cache[(r, c)]
         qls.append(q)
         nnzs.append(nz)
@@ -158,7 +161,10 @@ def main():
     ap.add_argument("--tokens", type=int, default=3)
     ap.add_argument("--rotation", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1, help="sequences decoded together (1..16)")
+    ap.add_argument("--sparsity", type=float, default=0.0045, help="CSR outlier density")
     args = ap.parse_args()
+    global SPARSITY_ARG
+    SPARSITY_ARG = args.sparsity
     try:
         peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except Exception:
